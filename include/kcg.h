@@ -1,0 +1,142 @@
+/* kcg — B200-native arb-count (k-clique counting) C ABI.
+ *
+ * This is the drop-in boundary: a C-ABI shared library
+ * (paper_2002_10047_b200/lib/libkcg.so, sm_100a) with plain pointers and
+ * sizes.  The C++ library libkclique_b200.so implements the reference's own
+ * entry points (the headers in include/kclique/, mirroring
+ * /root/reference/proj/include/kclique/) on top of these calls; any other
+ * host language binds them directly.
+ *
+ * Conventions
+ *  - Every call returns a status: KCG_OK, KCG_EINVAL (the cases where the
+ *    reference throws std::invalid_argument), KCG_ERUNTIME (CUDA/runtime
+ *    failure), KCG_ENOMEM (device or host allocation failed).
+ *    kcg_last_error() returns the calling thread's last message.
+ *  - Host buffers are caller-allocated; device memory is owned by the
+ *    kcg_graph handle and stays resident across calls.
+ *  - A handle is not internally synchronised: use one handle per host
+ *    thread (each handle owns its own CUDA stream), or serialise calls.
+ *  - All counts are uint64 and wrap modulo 2^64 like the reference
+ *    (SPEC.md:225).
+ *  - There is no CPU fallback: without a usable sm_100 device every
+ *    compute call fails with KCG_ERUNTIME.
+ */
+#ifndef KCG_H_
+#define KCG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KCG_OK 0
+#define KCG_EINVAL 1
+#define KCG_ERUNTIME 2
+#define KCG_ENOMEM 3
+
+/* OrientStrategy (proj/include/kclique/orientation.hpp:10-16), same order. */
+#define KCG_DEGREE 0
+#define KCG_ORIGINAL 1
+#define KCG_KCORE 2
+#define KCG_GOODRICH_PSZONA 3
+#define KCG_BARENBOIM_ELKIN 4
+
+typedef struct kcg_graph kcg_graph;
+
+/* Device-timed phase split of the most recent calls on a handle, in ms
+ * (CUDA events on the handle's stream), plus transfer bytes. */
+typedef struct kcg_times {
+  double upload_ms;   /* H2D of the input CSR (kcg_graph_create) */
+  double rank_ms;     /* last kcg_rank / kcg_estimate_arboricity */
+  double direct_ms;   /* last kcg_direct (DAG + relabelled DAG build) */
+  double count_ms;    /* last kcg_count, all counting kernels */
+  double count_kernel_ms; /* the dominant counting kernel(s) only */
+  double download_ms; /* D2H of the last call's host outputs */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+} kcg_times;
+
+/* Static description of the counting work of the last kcg_count. */
+typedef struct kcg_count_stats {
+  uint64_t sources_warp;   /* sources with out-degree <= 32 */
+  uint64_t sources_cta;    /* 32 < out-degree <= smem tier limit */
+  uint64_t sources_heavy;  /* beyond the shared-memory limit */
+  uint64_t max_out_degree;
+  uint64_t staged_elems;   /* adjacency entries read while staging */
+  uint64_t launches;       /* kernels launched by the last kcg_count */
+} kcg_count_stats;
+
+const char* kcg_last_error(void);
+const char* kcg_version(void);
+
+/* Device properties this library sizes itself from. */
+int kcg_device_info(int* sm_count, int* smem_optin_bytes, int* l2_bytes,
+                    int* cc_major, int* cc_minor);
+
+/* Uploads an undirected simple CSR (kclique::Graph layout,
+ * graph.hpp:59-62: u64 offsets[n+1], u32 adjacency[2m], ascending,
+ * symmetric, loop-free).  Replaces the Graph the reference's entry points
+ * take by const reference.  Host pointers. */
+int kcg_graph_create(uint32_t n, const uint64_t* offsets, const uint32_t* adj,
+                     kcg_graph** out);
+/* Same from device-resident arrays (copied on the handle's stream). */
+int kcg_graph_create_device(uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                            const uint32_t* d_adj, kcg_graph** out);
+/* Adopts an already-oriented DAG (kclique::DirectedGraph layout,
+ * graph.hpp:91-121: out_offsets[n+1], out-targets[m] ascending by id) and
+ * its ranking, for count_total/count_per_vertex on a DirectedGraph that
+ * did not come from this handle.  rank may be NULL only if n == 0. */
+int kcg_dag_create(uint32_t n, const uint64_t* out_offsets,
+                   const uint32_t* out_targets, const uint32_t* rank,
+                   kcg_graph** out);
+void kcg_graph_destroy(kcg_graph* g);
+uint32_t kcg_num_vertices(const kcg_graph* g);
+uint64_t kcg_num_edges(const kcg_graph* g);
+
+/* Ranking (orientation.cpp:10-174).  strategy is one of KCG_*; for
+ * KCG_BARENBOIM_ELKIN an alpha_hat of 0 means "estimate it with
+ * estimate_arboricity(g, eps)" exactly as make_ranking does
+ * (orientation.cpp:167-170).  The ranking stays on the device for
+ * kcg_direct.  rank_out (n entries), rounds_out and alpha_out may be NULL.
+ * KCG_EINVAL for eps <= 0 (peeling strategies) or an unknown strategy. */
+int kcg_rank(kcg_graph* g, int strategy, double eps, uint64_t alpha_hat,
+             uint32_t* rank_out, uint64_t* rounds_out, uint64_t* alpha_out);
+/* estimate_arboricity (orientation.cpp:124-155). */
+int kcg_estimate_arboricity(kcg_graph* g, double eps, uint64_t* out);
+/* Installs a host ranking; KCG_EINVAL unless it is a bijection onto [0,n)
+ * (graph.cpp:48-55) of length n (graph.cpp:95-96). */
+int kcg_set_ranking(kcg_graph* g, const uint32_t* rank, uint32_t len);
+
+/* direct_by_ranking (graph.cpp:94-114) on the device with the handle's
+ * current ranking.  Outputs are optional host buffers: out_offsets
+ * (n+1), out_targets (m); max_out_degree may be NULL. */
+int kcg_direct(kcg_graph* g, uint64_t* out_offsets, uint32_t* out_targets,
+               uint64_t* max_out_degree);
+
+/* count_total / count_per_vertex (counting.cpp:85-212) on the handle's
+ * DAG (built by kcg_direct or adopted by kcg_dag_create).  per_vertex is
+ * NULL for totals only, else n entries indexed by vertex id.
+ * KCG_EINVAL for k < 2. */
+int kcg_count(kcg_graph* g, int k, uint64_t* total, uint64_t* per_vertex);
+/* Device pointer to the per-vertex counts of the last per-vertex count
+ * (n u64, vertex-id order); valid until the next call on the handle. */
+int kcg_per_vertex_device(kcg_graph* g, const uint64_t** d_per_vertex);
+
+/* Fused rank -> direct -> count with no host round trip in between
+ * (the benchmark's step).  per_vertex may be NULL. */
+int kcg_pipeline(kcg_graph* g, int strategy, double eps, uint64_t alpha_hat,
+                 int k, uint64_t* total, uint64_t* per_vertex);
+
+int kcg_timings(const kcg_graph* g, kcg_times* out);
+int kcg_last_count_stats(const kcg_graph* g, kcg_count_stats* out);
+/* Bytes of device memory the handle currently holds. */
+uint64_t kcg_device_bytes(const kcg_graph* g);
+/* Blocks until all work queued on the handle's stream is done. */
+int kcg_synchronize(kcg_graph* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KCG_H_ */

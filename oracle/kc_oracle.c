@@ -1,0 +1,310 @@
+/* TEST INFRASTRUCTURE ONLY — the CPU restatement ("port") oracle.
+ *
+ * Plain-C restatement of the reference's arb-count path, used by tests/ as
+ * the checker and by bench.py's cpu_baseline leg when the compiled
+ * reference (oracle/_ref/libkclique_ref.so) is absent.  Nothing in the
+ * product links, loads or calls this file.
+ *
+ * Pinned by tests/test_oracle_pin.py against (1) the compiled reference
+ * itself on hundreds of seeded graphs, and (2) the reference's own known
+ * answers (proj/tests/test_counting.cpp:30-46, test_orientation.cpp:54-185).
+ *
+ * Each function cites the reference file:line it restates; paths are
+ * relative to /root/reference/proj.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- ranking -------------------------------------------------------- */
+
+/* rank_by_degree, src/orientation.cpp:10-17: stable sort of ids by degree
+ * (ties keep id order), restated as a counting sort. */
+int kco_rank_degree(uint32_t n, const uint64_t* off, uint32_t* rank) {
+  uint64_t maxd = 0;
+  for (uint32_t v = 0; v < n; v++)
+    if (off[v + 1] - off[v] > maxd) maxd = off[v + 1] - off[v];
+  uint64_t* start = calloc(maxd + 2, sizeof(uint64_t));
+  if (!start) return 3;
+  for (uint32_t v = 0; v < n; v++) start[off[v + 1] - off[v] + 1]++;
+  for (uint64_t d = 0; d <= maxd; d++) start[d + 1] += start[d];
+  for (uint32_t v = 0; v < n; v++) rank[v] = (uint32_t)start[off[v + 1] - off[v]]++;
+  free(start);
+  return 0;
+}
+
+/* estimate_arboricity, src/orientation.cpp:124-155.  Batch members are
+ * processed in id order; each one's alive neighbours lose a degree and an
+ * edge before the member itself dies, so intra-batch edges count once. */
+int kco_estimate_arboricity(uint32_t n, uint64_t m, const uint64_t* off,
+                            const uint32_t* adj, double eps, uint64_t* out) {
+  if (!(eps > 0)) return 1;
+  uint64_t* deg = malloc((size_t)n * 8 + 8);
+  uint8_t* alive = malloc((size_t)n + 1);
+  uint32_t* rem = malloc((size_t)n * 4 + 4);
+  uint32_t* batch = malloc((size_t)n * 4 + 4);
+  if (!deg || !alive || !rem || !batch) return 3;
+  for (uint32_t v = 0; v < n; v++) {
+    deg[v] = off[v + 1] - off[v];
+    alive[v] = 1;
+    rem[v] = v;
+  }
+  uint64_t nrem = n, edges_left = m;
+  double peak = 0;
+  while (nrem) {
+    double density = (double)edges_left / (double)nrem;
+    if (density > peak) peak = density;
+    double cutoff = 2 * (1 + eps) * density;
+    uint64_t nb = 0;
+    for (uint64_t i = 0; i < nrem; i++)
+      if ((double)deg[rem[i]] <= cutoff) batch[nb++] = rem[i];
+    for (uint64_t i = 0; i < nb; i++) {
+      uint32_t v = batch[i];
+      for (uint64_t p = off[v]; p < off[v + 1]; p++)
+        if (alive[adj[p]]) {
+          deg[adj[p]]--;
+          edges_left--;
+        }
+      alive[v] = 0;
+    }
+    uint64_t w = 0;
+    for (uint64_t i = 0; i < nrem; i++)
+      if (alive[rem[i]]) rem[w++] = rem[i];
+    nrem = w;
+  }
+  uint64_t a = (uint64_t)ceil(peak);
+  *out = a < 1 ? 1 : a;
+  free(deg), free(alive), free(rem), free(batch);
+  return 0;
+}
+
+/* rank_barenboim_elkin, src/orientation.cpp:86-122: each round removes
+ * every remaining vertex with double(deg) < threshold, in id order; an
+ * empty round doubles the threshold and still counts as a round;
+ * decrements apply only to survivors of the round. */
+int kco_rank_be(uint32_t n, const uint64_t* off, const uint32_t* adj,
+                double eps, uint64_t alpha_hat, uint32_t* rank,
+                uint64_t* rounds_out) {
+  if (!(eps > 0)) return 1;
+  if (alpha_hat < 1) return 1;
+  uint64_t* deg = malloc((size_t)n * 8 + 8);
+  uint8_t* alive = malloc((size_t)n + 1);
+  uint32_t* rem = malloc((size_t)n * 4 + 4);
+  uint32_t* batch = malloc((size_t)n * 4 + 4);
+  if (!deg || !alive || !rem || !batch) return 3;
+  for (uint32_t v = 0; v < n; v++) {
+    deg[v] = off[v + 1] - off[v];
+    alive[v] = 1;
+    rem[v] = v;
+  }
+  double threshold = (2 + eps) * (double)alpha_hat;
+  uint64_t nrem = n, rounds = 0, placed = 0;
+  while (nrem) {
+    rounds++;
+    uint64_t nb = 0;
+    for (uint64_t i = 0; i < nrem; i++)
+      if ((double)deg[rem[i]] < threshold) batch[nb++] = rem[i];
+    if (nb == 0) {
+      threshold *= 2;
+      continue;
+    }
+    for (uint64_t i = 0; i < nb; i++) {
+      rank[batch[i]] = (uint32_t)placed++;
+      alive[batch[i]] = 0;
+    }
+    for (uint64_t i = 0; i < nb; i++)
+      for (uint64_t p = off[batch[i]]; p < off[batch[i] + 1]; p++)
+        if (alive[adj[p]]) deg[adj[p]]--;
+    uint64_t w = 0;
+    for (uint64_t i = 0; i < nrem; i++)
+      if (alive[rem[i]]) rem[w++] = rem[i];
+    nrem = w;
+  }
+  if (rounds_out) *rounds_out = rounds;
+  free(deg), free(alive), free(rem), free(batch);
+  return 0;
+}
+
+/* rank_by_kcore, src/orientation.cpp:23-46: lazy-deletion min-heap on
+ * (induced degree, id); pops one vertex at a time. */
+typedef struct { uint64_t d; uint32_t v; } kco_entry;
+static int entry_less(kco_entry a, kco_entry b) {
+  return a.d < b.d || (a.d == b.d && a.v < b.v);
+}
+int kco_rank_kcore(uint32_t n, const uint64_t* off, const uint32_t* adj,
+                   uint32_t* rank) {
+  uint64_t cap = (uint64_t)n + (n ? off[n] : 0) + 1, size = 0;
+  kco_entry* heap = malloc(cap * sizeof(kco_entry));
+  uint64_t* deg = malloc((size_t)n * 8 + 8);
+  uint8_t* done = calloc((size_t)n + 1, 1);
+  if (!heap || !deg || !done) return 3;
+#define KCO_PUSH(D, V)                                                  \
+  do {                                                                  \
+    kco_entry e_ = {(D), (V)};                                          \
+    uint64_t i_ = size++;                                               \
+    while (i_ && entry_less(e_, heap[(i_ - 1) / 2])) {                  \
+      heap[i_] = heap[(i_ - 1) / 2];                                    \
+      i_ = (i_ - 1) / 2;                                                \
+    }                                                                   \
+    heap[i_] = e_;                                                      \
+  } while (0)
+  for (uint32_t v = 0; v < n; v++) {
+    deg[v] = off[v + 1] - off[v];
+    KCO_PUSH(deg[v], v);
+  }
+  uint32_t placed = 0;
+  while (size) {
+    kco_entry top = heap[0];
+    kco_entry last = heap[--size];
+    uint64_t i = 0;
+    for (;;) {
+      uint64_t c = 2 * i + 1;
+      if (c >= size) break;
+      if (c + 1 < size && entry_less(heap[c + 1], heap[c])) c++;
+      if (!entry_less(heap[c], last)) break;
+      heap[i] = heap[c];
+      i = c;
+    }
+    if (size) heap[i] = last;
+    if (done[top.v] || top.d != deg[top.v]) continue;
+    done[top.v] = 1;
+    rank[top.v] = placed++;
+    for (uint64_t p = off[top.v]; p < off[top.v + 1]; p++) {
+      uint32_t u = adj[p];
+      if (!done[u]) {
+        deg[u]--;
+        KCO_PUSH(deg[u], u);
+      }
+    }
+  }
+#undef KCO_PUSH
+  free(heap), free(deg), free(done);
+  return 0;
+}
+
+/* ---- orientation ---------------------------------------------------- */
+
+/* direct_by_ranking, src/graph.cpp:94-114: keep u->v iff rank(v) >
+ * rank(u); slices keep the undirected slice's ascending id order.
+ * out_off has n+1 entries, out_adj m entries. */
+int kco_direct(uint32_t n, const uint64_t* off, const uint32_t* adj,
+               const uint32_t* rank, uint64_t* out_off, uint32_t* out_adj) {
+  out_off[0] = 0;
+  uint64_t pos = 0;
+  for (uint32_t u = 0; u < n; u++) {
+    for (uint64_t p = off[u]; p < off[u + 1]; p++)
+      if (rank[adj[p]] > rank[u]) out_adj[pos++] = adj[p];
+    out_off[u + 1] = pos;
+  }
+  return 0;
+}
+
+/* ---- counting ------------------------------------------------------- */
+
+typedef struct {
+  const uint64_t* off;
+  const uint32_t* adj;
+  uint64_t* stamp;   /* per-vertex token marks (clique_rec.hpp:24-62) */
+  uint32_t** bufs;   /* candidate buffers per depth */
+  uint64_t* pv;      /* may be NULL */
+  uint32_t* chain;
+  int chain_len;
+} kco_ctx;
+
+/* clique_rec, src/clique_rec.hpp:24-62, in global id space with the
+ * stamp array (edge engine, src/counting.cpp:174-186). */
+static uint64_t kco_rec(kco_ctx* c, const uint32_t* cands, uint64_t ncand,
+                        int remaining, int depth, uint64_t token_base) {
+  if (ncand < (uint64_t)remaining) return 0;
+  if (remaining == 1) {
+    if (c->pv) {
+      for (uint64_t i = 0; i < ncand; i++) c->pv[cands[i]]++;
+      for (int i = 0; i < c->chain_len; i++) c->pv[c->chain[i]] += ncand;
+    }
+    return ncand;
+  }
+  const uint64_t token = token_base + (uint64_t)depth;
+  uint64_t total = 0;
+  uint32_t* next = c->bufs[depth + 1];
+  for (uint64_t i = 0; i < ncand; i++) {
+    uint32_t u = cands[i];
+    uint64_t nn = 0;
+    for (uint64_t p = c->off[u]; p < c->off[u + 1]; p++)
+      if (c->stamp[c->adj[p]] == token) next[nn++] = c->adj[p];
+    if (nn + 1 < (uint64_t)remaining) continue;
+    for (uint64_t j = 0; j < nn; j++) c->stamp[next[j]] = token + 1;
+    c->chain[c->chain_len++] = u;
+    total += kco_rec(c, next, nn, remaining - 1, depth + 1, token_base);
+    c->chain_len--;
+    for (uint64_t j = 0; j < nn; j++) c->stamp[next[j]] = token;
+  }
+  return total;
+}
+
+/* count_impl edge engine, src/counting.cpp:138-189 (serial): one task per
+ * directed edge (v,u); candidates = N+(v) ∩ N+(u) by sorted merge; k==2
+ * special case.  pv (n entries) may be NULL.  Returns 1 for k < 2. */
+int kco_count(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
+              int k, uint64_t* total_out, uint64_t* pv) {
+  if (k < 2) return 1;
+  uint64_t maxd = 0;
+  for (uint32_t v = 0; v < n; v++)
+    if (out_off[v + 1] - out_off[v] > maxd) maxd = out_off[v + 1] - out_off[v];
+  kco_ctx c;
+  c.off = out_off;
+  c.adj = out_adj;
+  c.pv = pv;
+  c.stamp = calloc((size_t)n + 1, 8);
+  c.chain = malloc(((size_t)k + 2) * 4);
+  c.bufs = malloc(((size_t)k + 3) * sizeof(uint32_t*));
+  if (!c.stamp || !c.chain || !c.bufs) return 3;
+  for (int i = 0; i < k + 3; i++) {
+    c.bufs[i] = malloc((maxd + 1) * 4);
+    if (!c.bufs[i]) return 3;
+  }
+  if (pv) memset(pv, 0, (size_t)n * 8);
+  uint64_t total = 0, next_token = 1;
+  for (uint32_t v = 0; v < n; v++) {
+    for (uint64_t e = out_off[v]; e < out_off[v + 1]; e++) {
+      uint32_t u = out_adj[e];
+      if (k == 2) {
+        total++;
+        if (pv) pv[v]++, pv[u]++;
+        continue;
+      }
+      /* std::set_intersection of two id-sorted slices (counting.cpp:178) */
+      uint32_t* both = c.bufs[2];
+      uint64_t nb = 0, a = out_off[v], b = out_off[u];
+      while (a < out_off[v + 1] && b < out_off[u + 1]) {
+        if (out_adj[a] < out_adj[b]) a++;
+        else if (out_adj[b] < out_adj[a]) b++;
+        else { both[nb++] = out_adj[a]; a++; b++; }
+      }
+      if (nb + 2 < (uint64_t)k) continue;
+      uint64_t tb = next_token;
+      next_token += (uint64_t)k + 2;
+      for (uint64_t i = 0; i < nb; i++) c.stamp[both[i]] = tb + 2;
+      c.chain[0] = v;
+      c.chain[1] = u;
+      c.chain_len = 2;
+      total += kco_rec(&c, both, nb, k - 2, 2, tb);
+    }
+  }
+  *total_out = total;
+  for (int i = 0; i < k + 3; i++) free(c.bufs[i]);
+  free(c.bufs), free(c.chain), free(c.stamp);
+  return 0;
+}
+
+/* Closed-form algorithmic staging bytes of the paper's per-source scheme
+ * (SURVEY.md §8(d)): 16n + 20m + 4 * sum_w indeg(w) * outdeg(w). */
+uint64_t kco_alg_bytes(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj) {
+  uint64_t m = n ? out_off[n] : 0;
+  uint64_t* indeg = calloc((size_t)n + 1, 8);
+  for (uint64_t e = 0; e < m; e++) indeg[out_adj[e]]++;
+  uint64_t s = 0;
+  for (uint32_t w = 0; w < n; w++) s += indeg[w] * (out_off[w + 1] - out_off[w]);
+  free(indeg);
+  return 16 * (uint64_t)n + 20 * m + 4 * s;
+}

@@ -1,0 +1,52 @@
+// RAII wrapper over the kcg C ABI, shared by the drop-in translation units.
+// Status codes map back onto the reference's exception types
+// (SURVEY.md §8(b)): KCG_EINVAL -> std::invalid_argument,
+// KCG_ENOMEM -> std::bad_alloc, anything else -> std::runtime_error.
+#pragma once
+
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "kcg.h"
+#include "kclique/graph.hpp"
+
+namespace kclique::b200 {
+
+inline void check(int rc) {
+  if (rc == KCG_OK) return;
+  std::string msg = kcg_last_error();
+  if (rc == KCG_EINVAL) throw std::invalid_argument(msg);
+  if (rc == KCG_ENOMEM) throw std::bad_alloc();
+  throw std::runtime_error("kcg: " + msg);
+}
+
+class Handle {
+ public:
+  explicit Handle(kcg_graph* h) : h_(h) {}
+  Handle(const Handle&) = delete;
+  Handle& operator=(const Handle&) = delete;
+  ~Handle() { kcg_graph_destroy(h_); }
+  kcg_graph* get() const { return h_; }
+
+  static Handle upload(const Graph& g) {
+    kcg_graph* h = nullptr;
+    check(kcg_graph_create(g.num_vertices(), g.offsets().data(), g.adjacency().data(), &h));
+    return Handle(h);
+  }
+  static Handle adopt(const DirectedGraph& dg) {
+    kcg_graph* h = nullptr;
+    std::vector<uint64_t> off(size_t(dg.num_vertices()) + 1);
+    for (VertexId v = 0; v < dg.num_vertices(); v++) off[v] = dg.out_offset(v);
+    off[dg.num_vertices()] = dg.num_edges();
+    check(kcg_dag_create(dg.num_vertices(), off.data(), dg.out_targets().data(),
+                         dg.ranking().ranks().data(), &h));
+    return Handle(h);
+  }
+  Handle(Handle&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+
+ private:
+  kcg_graph* h_;
+};
+
+}  // namespace kclique::b200

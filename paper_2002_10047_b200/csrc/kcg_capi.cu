@@ -1,0 +1,443 @@
+// extern "C" surface of libkcg.so (include/kcg.h): handle lifecycle,
+// transfers, status-code mapping.  The compute phases live in
+// kcg_rank.cu, kcg_direct.cu and kcg_count.cu.
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "kcg_internal.cuh"
+
+namespace kcg {
+
+namespace {
+thread_local std::string g_last_error;
+std::once_flag g_dev_once;
+Device g_dev;
+bool g_dev_ok = false;
+std::string g_dev_err;
+
+__global__ void degree_kernel(const uint64_t* __restrict__ off, uint32_t n,
+                              uint32_t* __restrict__ deg) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x)
+    deg[v] = uint32_t(off[v + 1] - off[v]);
+}
+
+// Validates a bijection: seen[r] counts hits; any r >= n or a repeat
+// raises the flag.
+__global__ void bijection_kernel(const uint32_t* __restrict__ rank, uint32_t n,
+                                 uint32_t* __restrict__ seen,
+                                 uint32_t* __restrict__ order,
+                                 unsigned long long* __restrict__ bad) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x) {
+    uint32_t r = rank[v];
+    if (r >= n || atomicAdd(&seen[r], 1u) != 0) {
+      atomicAdd(bad, 1ull);
+    } else {
+      order[r] = v;
+    }
+  }
+}
+
+}  // namespace
+
+void fail(int status, const std::string& msg) { throw Error(status, msg); }
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+const Device& device() {
+  std::call_once(g_dev_once, [] {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+      g_dev_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+      (void)cudaGetLastError();
+      return;
+    }
+    cudaDeviceProp p;
+    e = cudaGetDeviceProperties(&p, dev);
+    if (e != cudaSuccess) {
+      g_dev_err = cudaGetErrorString(e);
+      (void)cudaGetLastError();
+      return;
+    }
+    g_dev.id = dev;
+    g_dev.sms = p.multiProcessorCount;
+    g_dev.smem_optin = int(p.sharedMemPerBlockOptin);
+    g_dev.l2 = p.l2CacheSize;
+    g_dev.major = p.major;
+    g_dev.minor = p.minor;
+    if (p.major != 10) {
+      g_dev_err = "libkcg is built for sm_100a (B200); found compute capability " +
+                  std::to_string(p.major) + "." + std::to_string(p.minor);
+      return;
+    }
+    g_dev_ok = true;
+  });
+  if (!g_dev_ok) fail(KCG_ERUNTIME, g_dev_err);
+  return g_dev;
+}
+
+Graph::Graph() {
+  device();
+  KCG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  for (auto& e : ev) KCG_CUDA(cudaEventCreate(&e));
+}
+
+Graph::~Graph() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Graph::sync() { KCG_CUDA(cudaStreamSynchronize(stream)); }
+
+double Graph::elapsed(int a, int b) {
+  float ms = 0;
+  KCG_CUDA(cudaEventSynchronize(ev[b]));
+  KCG_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+  return ms;
+}
+
+void* cub_temp(Graph& g, size_t bytes) { return g.scratch.ensure(bytes, &g.bytes); }
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return KCG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return KCG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return KCG_ERUNTIME;
+  }
+}
+
+Graph* G(kcg_graph* h) {
+  if (!h) fail(KCG_EINVAL, "null kcg_graph handle");
+  return reinterpret_cast<Graph*>(h);
+}
+const Graph* G(const kcg_graph* h) {
+  if (!h) fail(KCG_EINVAL, "null kcg_graph handle");
+  return reinterpret_cast<const Graph*>(h);
+}
+
+// Copies host -> device through a pinned staging buffer when the source is
+// pageable (one cudaMemcpyAsync per chunk).
+void upload(Graph& g, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  cudaPointerAttributes attr;
+  bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
+                attr.type == cudaMemoryTypeHost;
+  (void)cudaGetLastError();
+  if (pinned) {
+    KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
+  } else {
+    KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
+  }
+  g.times.h2d_bytes += bytes;
+}
+
+void download(Graph& g, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g.stream));
+  g.times.d2h_bytes += bytes;
+}
+
+void finish_und(Graph& g) {
+  g.deg.ensure(g.n, &g.bytes);
+  if (g.n)
+    degree_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.und_off.p, g.n, g.deg.p);
+  KCG_LAUNCH_CHECK();
+  g.has_und = true;
+}
+
+void install_rank_device(Graph& g) {
+  // rank[] already on device: validate and build order[]
+  uint32_t* seen = reinterpret_cast<uint32_t*>(g.scratch2.ensure(size_t(g.n) * 4 + 8, &g.bytes));
+  g.counters.ensure(4, &g.bytes);
+  KCG_CUDA(cudaMemsetAsync(seen, 0, size_t(g.n) * 4, g.stream));
+  KCG_CUDA(cudaMemsetAsync(g.counters.p, 0, 8, g.stream));
+  g.order.ensure(g.n, &g.bytes);
+  if (g.n)
+    bijection_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.rank.p, g.n, seen,
+                                                                   g.order.p, g.counters.p);
+  KCG_LAUNCH_CHECK();
+  unsigned long long bad = 0;
+  KCG_CUDA(cudaMemcpyAsync(&bad, g.counters.p, 8, cudaMemcpyDeviceToHost, g.stream));
+  g.sync();
+  if (bad) fail(KCG_EINVAL, "ranking is not a bijection");
+  g.has_rank = true;
+  g.has_dag = g.has_rdag = false;
+}
+
+}  // namespace
+}  // namespace kcg
+
+using namespace kcg;
+
+extern "C" {
+
+const char* kcg_last_error(void) { return g_last_error.c_str(); }
+const char* kcg_version(void) { return "kcg 0.1 sm_100a"; }
+
+int kcg_device_info(int* sm_count, int* smem_optin_bytes, int* l2_bytes, int* cc_major,
+                    int* cc_minor) {
+  return guarded([&] {
+    const Device& d = device();
+    if (sm_count) *sm_count = d.sms;
+    if (smem_optin_bytes) *smem_optin_bytes = d.smem_optin;
+    if (l2_bytes) *l2_bytes = d.l2;
+    if (cc_major) *cc_major = d.major;
+    if (cc_minor) *cc_minor = d.minor;
+  });
+}
+
+int kcg_graph_create(uint32_t n, const uint64_t* offsets, const uint32_t* adj,
+                     kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    if (!offsets) fail(KCG_EINVAL, "offsets is null");
+    if (offsets[0] != 0) fail(KCG_EINVAL, "offsets[0] != 0");
+    uint64_t two_m = offsets[n];
+    if (two_m % 2) fail(KCG_EINVAL, "adjacency is not symmetric (odd length)");
+    if (two_m && !adj) fail(KCG_EINVAL, "adj is null");
+    auto* g = new Graph();
+    try {
+      g->n = n;
+      g->m = two_m / 2;
+      g->times = kcg_times{};
+      g->mark(0);
+      g->und_off.ensure(size_t(n) + 1, &g->bytes);
+      g->und_adj.ensure(two_m, &g->bytes);
+      upload(*g, g->und_off.p, offsets, (size_t(n) + 1) * 8);
+      upload(*g, g->und_adj.p, adj, two_m * 4);
+      finish_und(*g);
+      g->mark(1);
+      g->times.upload_ms = g->elapsed(0, 1);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(g);
+  });
+}
+
+int kcg_graph_create_device(uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                            const uint32_t* d_adj, kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    auto* g = new Graph();
+    try {
+      g->n = n;
+      g->m = m;
+      g->und_off.ensure(size_t(n) + 1, &g->bytes);
+      g->und_adj.ensure(2 * m, &g->bytes);
+      KCG_CUDA(cudaMemcpyAsync(g->und_off.p, d_offsets, (size_t(n) + 1) * 8,
+                               cudaMemcpyDeviceToDevice, g->stream));
+      if (m)
+        KCG_CUDA(cudaMemcpyAsync(g->und_adj.p, d_adj, 2 * m * 4, cudaMemcpyDeviceToDevice,
+                                 g->stream));
+      finish_und(*g);
+      g->sync();
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(g);
+  });
+}
+
+int kcg_dag_create(uint32_t n, const uint64_t* out_offsets, const uint32_t* out_targets,
+                   const uint32_t* rank, kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    if (!out_offsets) fail(KCG_EINVAL, "out_offsets is null");
+    if (n && !rank) fail(KCG_EINVAL, "rank is null");
+    uint64_t m = out_offsets[n];
+    if (m && !out_targets) fail(KCG_EINVAL, "out_targets is null");
+    auto* g = new Graph();
+    try {
+      g->n = n;
+      g->m = m;
+      g->times = kcg_times{};
+      g->mark(0);
+      g->dag_off.ensure(size_t(n) + 1, &g->bytes);
+      g->dag_adj.ensure(m, &g->bytes);
+      g->rank.ensure(n, &g->bytes);
+      upload(*g, g->dag_off.p, out_offsets, (size_t(n) + 1) * 8);
+      upload(*g, g->dag_adj.p, out_targets, m * 4);
+      upload(*g, g->rank.p, rank, size_t(n) * 4);
+      g->mark(1);
+      g->times.upload_ms = g->elapsed(0, 1);
+      install_rank_device(*g);
+      g->has_dag = true;
+      relabel_from_dag(*g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(g);
+  });
+}
+
+void kcg_graph_destroy(kcg_graph* h) {
+  try {
+    delete reinterpret_cast<Graph*>(h);
+  } catch (...) {
+  }
+}
+
+uint32_t kcg_num_vertices(const kcg_graph* h) {
+  return h ? reinterpret_cast<const Graph*>(h)->n : 0;
+}
+uint64_t kcg_num_edges(const kcg_graph* h) {
+  return h ? reinterpret_cast<const Graph*>(h)->m : 0;
+}
+
+int kcg_rank(kcg_graph* h, int strategy, double eps, uint64_t alpha_hat, uint32_t* rank_out,
+             uint64_t* rounds_out, uint64_t* alpha_out) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!g.has_und) fail(KCG_EINVAL, "handle holds no undirected graph");
+    g.times.d2h_bytes = 0;
+    uint64_t rounds = rank_graph(g, strategy, eps, alpha_hat, alpha_out);
+    g.has_rank = true;
+    g.has_dag = g.has_rdag = false;
+    if (rank_out) {
+      g.mark(4);
+      download(g, rank_out, g.rank.p, size_t(g.n) * 4);
+      g.mark(5);
+      g.sync();
+      g.times.download_ms = g.elapsed(4, 5);
+    }
+    if (rounds_out) *rounds_out = rounds;
+  });
+}
+
+int kcg_estimate_arboricity(kcg_graph* h, double eps, uint64_t* out) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!g.has_und) fail(KCG_EINVAL, "handle holds no undirected graph");
+    uint64_t a = estimate_arboricity(g, eps);
+    if (out) *out = a;
+  });
+}
+
+int kcg_set_ranking(kcg_graph* h, const uint32_t* rank, uint32_t len) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (len != g.n) fail(KCG_EINVAL, "ranking size does not match graph");
+    if (g.n && !rank) fail(KCG_EINVAL, "rank is null");
+    g.rank.ensure(g.n, &g.bytes);
+    upload(g, g.rank.p, rank, size_t(g.n) * 4);
+    install_rank_device(g);
+  });
+}
+
+int kcg_direct(kcg_graph* h, uint64_t* out_offsets, uint32_t* out_targets,
+               uint64_t* max_out_degree) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!g.has_rank) fail(KCG_EINVAL, "no ranking installed");
+    if (!g.has_und && !g.has_dag) fail(KCG_EINVAL, "handle holds no graph");
+    g.times.d2h_bytes = 0;
+    bool want_id = out_offsets || out_targets;
+    if (!g.has_rdag || (want_id && !g.has_dag)) build_dag(g, want_id);
+    g.mark(4);
+    if (out_offsets) download(g, out_offsets, g.dag_off.p, (size_t(g.n) + 1) * 8);
+    if (out_targets) download(g, out_targets, g.dag_adj.p, g.m * 4);
+    g.mark(5);
+    g.sync();
+    g.times.download_ms = g.elapsed(4, 5);
+    if (max_out_degree) *max_out_degree = g.max_out;
+  });
+}
+
+int kcg_count(kcg_graph* h, int k, uint64_t* total, uint64_t* per_vertex) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (!g.has_rdag) {
+      if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
+      build_dag(g, false);
+    }
+    g.times.d2h_bytes = 0;
+    uint64_t t = count_cliques(g, k, per_vertex != nullptr);
+    if (per_vertex) {
+      g.mark(4);
+      download(g, per_vertex, g.pv.p, size_t(g.n) * 8);
+      g.mark(5);
+      g.sync();
+      g.times.download_ms = g.elapsed(4, 5);
+    }
+    if (total) *total = t;
+  });
+}
+
+int kcg_per_vertex_device(kcg_graph* h, const uint64_t** d_per_vertex) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!d_per_vertex) fail(KCG_EINVAL, "null out pointer");
+    *d_per_vertex = g.pv.p;
+  });
+}
+
+int kcg_pipeline(kcg_graph* h, int strategy, double eps, uint64_t alpha_hat, int k,
+                 uint64_t* total, uint64_t* per_vertex) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (!g.has_und) fail(KCG_EINVAL, "handle holds no undirected graph");
+    g.times.d2h_bytes = 0;
+    rank_graph(g, strategy, eps, alpha_hat, nullptr);
+    g.has_rank = true;
+    g.has_dag = g.has_rdag = false;
+    build_dag(g, false);
+    uint64_t t = count_cliques(g, k, per_vertex != nullptr);
+    if (per_vertex) {
+      g.mark(4);
+      download(g, per_vertex, g.pv.p, size_t(g.n) * 8);
+      g.mark(5);
+      g.sync();
+      g.times.download_ms = g.elapsed(4, 5);
+    }
+    if (total) *total = t;
+  });
+}
+
+int kcg_timings(const kcg_graph* h, kcg_times* out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "null out pointer");
+    *out = G(h)->times;
+  });
+}
+
+int kcg_last_count_stats(const kcg_graph* h, kcg_count_stats* out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "null out pointer");
+    *out = G(h)->stats;
+  });
+}
+
+uint64_t kcg_device_bytes(const kcg_graph* h) {
+  return h ? reinterpret_cast<const Graph*>(h)->bytes : 0;
+}
+
+int kcg_synchronize(kcg_graph* h) {
+  return guarded([&] { G(h)->sync(); });
+}
+
+}  // extern "C"

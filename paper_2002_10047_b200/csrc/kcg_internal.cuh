@@ -1,0 +1,159 @@
+// Internal declarations shared by the kcg translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "kcg.h"
+
+namespace kcg {
+
+// ---- errors ----------------------------------------------------------------
+// Internal code throws; the extern "C" layer converts to status codes and
+// kcg_last_error().  Matches the reference's exception split
+// (std::invalid_argument -> KCG_EINVAL).
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] void fail(int status, const std::string& msg);
+void set_last_error(const std::string& msg);
+
+#define KCG_CUDA(call)                                                       \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      (void)cudaGetLastError();                                              \
+      ::kcg::fail(e_ == cudaErrorMemoryAllocation ? KCG_ENOMEM : KCG_ERUNTIME, \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    }                                                                        \
+  } while (0)
+#define KCG_LAUNCH_CHECK() KCG_CUDA(cudaGetLastError())
+
+// ---- device buffers ----------------------------------------------------------
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;     // elements allocated
+  size_t* acct = nullptr;  // byte accounting of the owning handle
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) {
+      cudaFree(p);
+      if (acct) *acct -= n * sizeof(T);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  // grows (never shrinks) to at least `count` elements; contents are lost
+  // when it grows
+  T* ensure(size_t count, size_t* account = nullptr) {
+    if (account) acct = account;
+    if (count <= n && p) return p;
+    release();
+    size_t c = count ? count : 1;
+    KCG_CUDA(cudaMalloc(&p, c * sizeof(T)));
+    n = c;
+    if (acct) *acct += n * sizeof(T);
+    return p;
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void* ensure(size_t b) {
+    if (b <= bytes && p) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    KCG_CUDA(cudaMallocHost(&p, b ? b : 1));
+    bytes = b;
+    return p;
+  }
+};
+
+struct Device {
+  int id = 0;
+  int sms = 148;
+  int smem_optin = 227 * 1024;
+  int l2 = 0;
+  int major = 0, minor = 0;
+};
+const Device& device();
+
+// ---- the graph handle --------------------------------------------------------
+// Whole graph resident in HBM.  Layouts:
+//   und_off/und_adj   undirected CSR (u64 offsets, u32 ids), ascending
+//   deg               undirected degree (u32)
+//   rank/order        rank[v], order[r] (u32)
+//   dag_off/dag_adj   id-space DAG, slices ascending by id (== reference)
+//   rdag_off/rdag_adj rank-relabelled DAG: vertex r = order[...], targets
+//                     are ranks, slices ascending -> every induced
+//                     subgraph is upper-triangular in local order
+//   pv_rank/pv        per-vertex counts by rank / by id
+struct Graph {
+  uint32_t n = 0;
+  uint64_t m = 0;
+  bool has_und = false;
+  bool has_rank = false;
+  bool has_dag = false;     // id-space DAG valid for current ranking
+  bool has_rdag = false;    // relabelled DAG valid for current ranking
+  uint64_t max_out = 0;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+
+  DevBuf<uint64_t> und_off;
+  DevBuf<uint32_t> und_adj;
+  DevBuf<uint32_t> deg;
+  DevBuf<uint32_t> rank, order;
+  DevBuf<uint64_t> dag_off;
+  DevBuf<uint32_t> dag_adj;
+  DevBuf<uint64_t> rdag_off;
+  DevBuf<uint32_t> rdag_adj;
+  DevBuf<uint64_t> pv_rank, pv;
+  DevBuf<unsigned char> scratch;   // CUB temp + misc
+  DevBuf<unsigned char> scratch2;  // per-call work arrays
+  DevBuf<unsigned char> heavy;     // heavy-tier global bitmaps
+  DevBuf<unsigned long long> counters;  // small device counters
+  PinnedBuf pinned;
+
+  kcg_times times{};
+  kcg_count_stats stats{};
+  cudaEvent_t ev[8] = {};
+
+  Graph();
+  ~Graph();
+  void sync();
+  // event-timed region on the handle's stream
+  void mark(int i) { KCG_CUDA(cudaEventRecord(ev[i], stream)); }
+  double elapsed(int a, int b);
+};
+
+// phases (kcg_rank.cu, kcg_direct.cu, kcg_count.cu)
+uint64_t estimate_arboricity(Graph& g, double eps);
+uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
+                    uint64_t* alpha_out);  // returns rounds
+void build_dag(Graph& g, bool want_id_dag);
+void relabel_from_dag(Graph& g);  // rdag from an adopted id-space DAG
+uint64_t count_cliques(Graph& g, int k, bool want_pv);
+
+// small helpers
+void* cub_temp(Graph& g, size_t bytes);
+inline unsigned blocks_for(uint64_t work, unsigned threads, unsigned cap = 148u * 32u) {
+  uint64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return unsigned(b);
+}
+
+}  // namespace kcg

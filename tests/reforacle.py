@@ -1,0 +1,228 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes bindings for the two oracles.
+
+* ``Ref``  — the UNMODIFIED reference library compiled from /root/reference
+  (oracle/_ref/libkclique_ref.so via oracle/Makefile + oracle/ref_capi.cpp).
+* ``Port`` — the plain-C restatement oracle/kc_oracle.c
+  (oracle/_ref/libkcoracle.so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg import
+this module, and only as the checker.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(os.path.dirname(_HERE), "oracle", "_ref")
+P = ctypes.POINTER
+c_u64p = ctypes.c_void_p
+
+
+def _arr(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class OracleError(Exception):
+    pass
+
+
+def _check(rc, what):
+    if rc == 1:
+        raise ValueError(f"{what}: invalid argument")
+    if rc != 0:
+        raise OracleError(f"{what}: status {rc}")
+
+
+class Ref:
+    """The compiled reference library."""
+
+    def __init__(self, path=None):
+        path = path or os.path.join(REF_DIR, "libkclique_ref.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        L.ref_graph_create.argtypes = [ctypes.c_uint32, vp, vp, P(vp)]
+        L.ref_graph_from_edge_list.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_uint64, P(vp)]
+        L.ref_graph_destroy.argtypes = [vp]
+        L.ref_graph_m.argtypes = [vp]
+        L.ref_graph_m.restype = ctypes.c_uint64
+        L.ref_graph_csr.argtypes = [vp, vp, vp]
+        L.ref_rank.argtypes = [vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64, vp,
+                               P(ctypes.c_uint64), P(ctypes.c_double)]
+        L.ref_estimate_arboricity.argtypes = [vp, ctypes.c_double, P(ctypes.c_uint64)]
+        L.ref_direct.argtypes = [vp, vp, P(vp), P(ctypes.c_double)]
+        L.ref_direct_sized.argtypes = [vp, vp, ctypes.c_uint32, P(vp)]
+        L.ref_dg_destroy.argtypes = [vp]
+        L.ref_dg_csr.argtypes = [vp, vp, vp]
+        L.ref_dg_max_out_degree.argtypes = [vp]
+        L.ref_dg_max_out_degree.restype = ctypes.c_uint64
+        L.ref_count.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                P(ctypes.c_uint64), vp, P(ctypes.c_double)]
+        L.ref_brute_force.argtypes = [vp, ctypes.c_int, P(ctypes.c_uint64), vp]
+        L.ref_exact_arboricity.argtypes = [vp, P(ctypes.c_uint64)]
+        L.ref_set_threads.argtypes = [ctypes.c_int]
+        self.L = L
+
+    def set_threads(self, t):
+        self.L.ref_set_threads(int(t))
+
+    def max_threads(self):
+        return int(self.L.ref_max_threads())
+
+    def graph(self, g):
+        h = ctypes.c_void_p()
+        off, adj = _arr(g.offsets, np.uint64), _arr(g.adj, np.uint32)
+        _check(self.L.ref_graph_create(g.n, off.ctypes.data, adj.ctypes.data, ctypes.byref(h)),
+               "graph")
+        return h
+
+    def graph_from_edges(self, n, edges):
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        us, vs = _arr(e[:, 0], np.uint32), _arr(e[:, 1], np.uint32)
+        h = ctypes.c_void_p()
+        _check(self.L.ref_graph_from_edge_list(n, us.ctypes.data, vs.ctypes.data, len(us),
+                                               ctypes.byref(h)), "from_edges")
+        return h
+
+    def graph_csr(self, h, n):
+        m = int(self.L.ref_graph_m(h))
+        off = np.zeros(n + 1, np.uint64)
+        adj = np.zeros(2 * m, np.uint32)
+        self.L.ref_graph_csr(h, off.ctypes.data, adj.ctypes.data)
+        return off, adj
+
+    def graph_digest(self, h, n):
+        from paper_2002_10047_b200 import gen
+        off, adj = self.graph_csr(h, n)
+        return f"{gen.digest_u64(off):016x}:{gen.digest_u32(adj):016x}"
+
+    def graph_destroy(self, h):
+        self.L.ref_graph_destroy(h)
+
+    def rank(self, h, n, strategy, eps=1.0, alpha_hat=0):
+        rank = np.zeros(n, np.uint32)
+        rounds = ctypes.c_uint64(0)
+        secs = ctypes.c_double(0)
+        _check(self.L.ref_rank(h, strategy, eps, alpha_hat, rank.ctypes.data,
+                               ctypes.byref(rounds), ctypes.byref(secs)), "rank")
+        return rank, int(rounds.value), float(secs.value)
+
+    def estimate_arboricity(self, h, eps):
+        out = ctypes.c_uint64(0)
+        _check(self.L.ref_estimate_arboricity(h, eps, ctypes.byref(out)), "estimate")
+        return int(out.value)
+
+    def direct(self, h, rank):
+        rank = _arr(rank, np.uint32)
+        dg = ctypes.c_void_p()
+        secs = ctypes.c_double(0)
+        _check(self.L.ref_direct(h, rank.ctypes.data, ctypes.byref(dg), ctypes.byref(secs)),
+               "direct")
+        return dg, float(secs.value)
+
+    def direct_sized(self, h, rank):
+        rank = _arr(rank, np.uint32)
+        dg = ctypes.c_void_p()
+        _check(self.L.ref_direct_sized(h, rank.ctypes.data, len(rank), ctypes.byref(dg)),
+               "direct")
+        return dg
+
+    def dg_csr(self, dg, n, m):
+        off = np.zeros(n + 1, np.uint64)
+        adj = np.zeros(m, np.uint32)
+        self.L.ref_dg_csr(dg, off.ctypes.data, adj.ctypes.data)
+        return off, adj
+
+    def dg_destroy(self, dg):
+        self.L.ref_dg_destroy(dg)
+
+    def count(self, dg, n, k, parallelism=2, build_induced=True, want_pv=False):
+        total = ctypes.c_uint64(0)
+        secs = ctypes.c_double(0)
+        pv = np.zeros(n if want_pv else 1, np.uint64)
+        _check(self.L.ref_count(dg, k, parallelism, int(build_induced), int(want_pv),
+                                ctypes.byref(total), pv.ctypes.data, ctypes.byref(secs)),
+               "count")
+        return int(total.value), (pv if want_pv else None), float(secs.value)
+
+    def brute_force(self, h, n, k):
+        total = ctypes.c_uint64(0)
+        pv = np.zeros(max(n, 1), np.uint64)
+        _check(self.L.ref_brute_force(h, k, ctypes.byref(total), pv.ctypes.data), "brute")
+        return int(total.value), pv[:n]
+
+    def exact_arboricity(self, h):
+        out = ctypes.c_uint64(0)
+        _check(self.L.ref_exact_arboricity(h, ctypes.byref(out)), "arboricity")
+        return int(out.value)
+
+
+class Port:
+    """The C restatement oracle/kc_oracle.c."""
+
+    def __init__(self, path=None):
+        path = path or os.path.join(REF_DIR, "libkcoracle.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        L.kco_rank_degree.argtypes = [ctypes.c_uint32, vp, vp]
+        L.kco_estimate_arboricity.argtypes = [ctypes.c_uint32, ctypes.c_uint64, vp, vp,
+                                              ctypes.c_double, P(ctypes.c_uint64)]
+        L.kco_rank_be.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_double, ctypes.c_uint64,
+                                  vp, P(ctypes.c_uint64)]
+        L.kco_rank_kcore.argtypes = [ctypes.c_uint32, vp, vp, vp]
+        L.kco_direct.argtypes = [ctypes.c_uint32, vp, vp, vp, vp, vp]
+        L.kco_count.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, P(ctypes.c_uint64), vp]
+        L.kco_alg_bytes.argtypes = [ctypes.c_uint32, vp, vp]
+        L.kco_alg_bytes.restype = ctypes.c_uint64
+        self.L = L
+
+    def rank_degree(self, g):
+        r = np.zeros(g.n, np.uint32)
+        _check(self.L.kco_rank_degree(g.n, _arr(g.offsets, np.uint64).ctypes.data,
+                                      r.ctypes.data), "rank_degree")
+        return r
+
+    def estimate_arboricity(self, g, eps):
+        out = ctypes.c_uint64(0)
+        _check(self.L.kco_estimate_arboricity(g.n, g.m, g.offsets.ctypes.data, g.adj.ctypes.data,
+                                              eps, ctypes.byref(out)), "estimate")
+        return int(out.value)
+
+    def rank_be(self, g, eps, alpha):
+        r = np.zeros(g.n, np.uint32)
+        rounds = ctypes.c_uint64(0)
+        _check(self.L.kco_rank_be(g.n, g.offsets.ctypes.data, g.adj.ctypes.data, eps, alpha,
+                                  r.ctypes.data, ctypes.byref(rounds)), "rank_be")
+        return r, int(rounds.value)
+
+    def rank_kcore(self, g):
+        r = np.zeros(g.n, np.uint32)
+        _check(self.L.kco_rank_kcore(g.n, g.offsets.ctypes.data, g.adj.ctypes.data,
+                                     r.ctypes.data), "rank_kcore")
+        return r
+
+    def direct(self, g, rank):
+        rank = _arr(rank, np.uint32)
+        off = np.zeros(g.n + 1, np.uint64)
+        adj = np.zeros(g.m, np.uint32)
+        self.L.kco_direct(g.n, g.offsets.ctypes.data, g.adj.ctypes.data, rank.ctypes.data,
+                          off.ctypes.data, adj.ctypes.data)
+        return off, adj
+
+    def count(self, n, off, adj, k, want_pv=False):
+        off, adj = _arr(off, np.uint64), _arr(adj, np.uint32)
+        total = ctypes.c_uint64(0)
+        pv = np.zeros(max(n, 1), np.uint64) if want_pv else None
+        _check(self.L.kco_count(n, off.ctypes.data, adj.ctypes.data, k, ctypes.byref(total),
+                                pv.ctypes.data if want_pv else None), "count")
+        return int(total.value), (pv[:n] if want_pv else None)
+
+    def alg_bytes(self, n, off, adj):
+        off, adj = _arr(off, np.uint64), _arr(adj, np.uint32)
+        return int(self.L.kco_alg_bytes(n, off.ctypes.data, adj.ctypes.data))
