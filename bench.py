@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""arb-count benchmark on B200 (contract: DESIGN.md §Measurement).
+
+Default workload = BASELINE.json configs[1]: R-MAT scale 20 (16,777,216
+samples, seed 2, permuted ids), Barenboim-Elkin ranking (eps = 0.5, alpha
+estimated), k = 4.  One step = one pass of the hot path over the graph
+resident in HBM: rank -> orient (DAG) -> count.  k = 5 on the same DAG is
+reported as a secondary measurement.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kcg|reference]
+                    [--config C] [--k K] [--no-cpu-baseline]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2002_10047_b200 import gen  # noqa: E402
+
+STRAT_NAMES = {0: "degree", 1: "original", 2: "kcore", 3: "goodrich_pszona",
+               4: "barenboim_elkin"}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["kcg", "reference"], default="kcg")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=240.0,
+                    help="wall budget for the reference arm's timed steps")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def workload(cfg_id, k):
+    spec = gen.CONFIGS[cfg_id]
+    k = k or spec["ks"][0]
+    return spec, k
+
+
+def config_obj(cfg_id, spec, k, g, extra=None):
+    c = {"workload": f"config{cfg_id}: {spec['desc']}", "k": k,
+         "strategy": STRAT_NAMES[spec["strategy"]], "eps": spec["eps"], "n": g.n, "m": g.m,
+         "step": "rank + orient (DAG) + count_total",
+         "l2": "flushed between timed steps (512 MiB memset on the library stream)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def alg_bytes(n, out_off, out_adj):
+    """B_alg = 16n + 20m + 4 * sum_w indeg(w) * outdeg(w)."""
+    outdeg = np.diff(out_off).astype(np.float64)
+    indeg = np.bincount(out_adj, minlength=n).astype(np.float64)
+    m = len(out_adj)
+    return 16.0 * n + 20.0 * m + 4.0 * float(np.dot(indeg, outdeg))
+
+
+def ncu_traffic(cfg_id, k):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        d = json.load(open(path))
+        ent = d.get(f"config{cfg_id}_k{k}")
+        return ent.get("dram_bytes_per_launch") if ent else None
+    except (ValueError, KeyError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference library)
+# ---------------------------------------------------------------------------
+def reference_step(R, rg, g, spec, k):
+    t0 = time.perf_counter()
+    rank, rounds, _ = R.rank(rg, g.n, spec["strategy"], spec["eps"], 0)
+    dg, _ = R.direct(rg, rank)
+    total, _, _ = R.count(dg, g.n, k, parallelism=2)
+    dt = time.perf_counter() - t0
+    R.dg_destroy(dg)
+    return total, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from tests import reforacle
+    spec, k = workload(args.config, args.k)
+    g = gen.load_config_graph(args.config, cache=False)
+    try:
+        R = reforacle.Ref()
+        kind = "reference"
+    except FileNotFoundError:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libkclique_ref.so not built"}))
+        return 0
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    rg = R.graph(g)
+    # first step doubles as warm-up and sizes the run to the budget
+    total, t_first = reference_step(R, rg, g, spec, k)
+    warm = max(0, min(args.warmup, 1) - 1)
+    for _ in range(warm):
+        reference_step(R, rg, g, spec, k)
+    steps = max(1, min(args.steps, int(args.cpu_budget_s // max(t_first, 1e-3))))
+    times = []
+    for _ in range(steps):
+        t, dt = reference_step(R, rg, g, spec, k)
+        assert t == total
+        times.append(dt)
+    sec = sum(times) / len(times)
+    value = total / sec
+    sample = (f"{steps} full step(s) of config {args.config} k={k} "
+              f"(rank+direct+count, OpenMP {cores} threads)")
+    print(json.dumps({
+        "impl": "reference", "metric": f"k-cliques/s (k={k})", "value": value,
+        "unit": "cliques/s", "n_gpus": world, "steps": steps, "warmup": 1 + warm,
+        "requested_steps": args.steps, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 ids / u64 counts",
+        "data": "synthetic (in-repo deterministic generator)",
+        "config": config_obj(args.config, spec, k, g),
+        "cpu_baseline": {"value": value, "unit": "cliques/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "cliques/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "total": str(total)}))
+    return 0
+
+
+def cpu_baseline(g, spec, k):
+    from tests import reforacle
+    try:
+        R = reforacle.Ref()
+        kind = "reference"
+    except FileNotFoundError:
+        return None
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    rg = R.graph(g)
+    total, dt = reference_step(R, rg, g, spec, k)
+    R.graph_destroy(rg)
+    return {"value": total / dt, "unit": "cliques/s", "cores": cores, "kind": kind,
+            "sample": f"one full step (rank+direct+count k={k}) on the same graph, "
+                      f"{dt:.2f} s", "total": str(total)}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_kcg(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_10047_b200 import kcg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec, k = workload(args.config, args.k)
+    strat, eps = spec["strategy"], spec["eps"]
+    g = gen.load_config_graph(args.config, cache=False)
+    h = kcg.DeviceGraph.from_graph(g)
+    stream = torch.cuda.ExternalStream(h.stream_ptr())
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        if world == 1:
+            return h.pipeline(strat, eps, k)[0]
+        h.rank(strat, eps, download=False)
+        h.direct(download=False)
+        return h.count_part(k, rank, world)[0]
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = h.timings()["launches"]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    phase = {"rank_ms": 0.0, "direct_ms": 0.0, "count_ms": 0.0, "count_kernel_ms": 0.0}
+    part_total = 0
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        ev[i][0].record(stream)
+        part_total = step()
+        ev[i][1].record(stream)
+        t = h.timings()
+        for key in phase:
+            phase[key] += t[key]
+    torch.cuda.synchronize()
+    launches = h.timings()["launches"] - launches0
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    total = part_total
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        ct = torch.tensor([part_total], dtype=torch.int64, device="cuda")
+        dist.all_reduce(ct)
+        total = int(ct.item()) % (1 << 64)
+        dist.barrier()
+    ms_per_step = ms / args.steps
+    value = total / (ms_per_step / 1e3)
+    for key in phase:
+        phase[key] /= args.steps
+    stats = h.count_stats()
+
+    # roofline of the dominant (counting) kernels
+    off, adj, max_out = h.direct()
+    b_alg = alg_bytes(g.n, off, adj)
+    peak, peak_src = measured_peaks()
+    achieved = b_alg / (phase["count_kernel_ms"] / 1e3) / 1e9
+    dag_bytes = 8 * (g.n + 1) + 4 * g.m
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(args.config, k),
+                "alg_bytes_per_launch": b_alg, "kernel_ms": phase["count_kernel_ms"],
+                "peak_source": peak_src,
+                "note": "achieved = B_alg (SURVEY.md §8(d): 16n+20m+4*sum indeg*outdeg) / "
+                        "device time of the counting kernels; the DAG (%.0f MB) %s L2"
+                        % (dag_bytes / 1e6, "fits in" if dag_bytes < 126e6 else "exceeds")}
+
+    # secondary: the config's other k values on the same DAG (counting only)
+    secondary = {}
+    if world == 1:
+        for k2 in spec["ks"]:
+            if k2 == k:
+                continue
+            h.rank(strat, eps, download=False)
+            h.direct(download=False)
+            reps = 3
+            tot2 = 0
+            cms = 0.0
+            for _ in range(reps):
+                tot2, _ = h.count(k2)
+                cms += h.timings()["count_ms"]
+            cms /= reps
+            secondary[f"k{k2}"] = {"total": str(tot2), "count_ms": cms,
+                                   "cliques_per_s": tot2 / (cms / 1e3),
+                                   "oriented_edges_per_s": g.m / (cms / 1e3)}
+
+    # e2e: the reference-facing C ABI with host buffers (pinned), H2D + D2H
+    # inside the timed region
+    e2e = None
+    if world == 1:
+        off_p = torch.from_numpy(g.offsets.view(np.int64)).pin_memory()
+        adj_p = torch.from_numpy(g.adj.view(np.int32)).pin_memory()
+        e_steps = max(1, min(args.steps, 5))
+        e_times = []
+        for _ in range(e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            he = kcg.DeviceGraph.from_csr_ptr(g.n, off_p.data_ptr(), adj_p.data_ptr())
+            te, _ = he.pipeline(strat, eps, k)
+            he.close()
+            e_times.append(time.perf_counter() - t0)
+            assert te == total
+        esec = sum(e_times) / len(e_times)
+        e2e = {"value": total / esec, "unit": "cliques/s",
+               "h2d_bytes_per_step": int(off_p.numel() * 8 + adj_p.numel() * 4),
+               "d2h_bytes_per_step": 8, "ms_per_step": esec * 1e3,
+               "path": "kcg_graph_create(pinned host CSR) + kcg_pipeline + destroy"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, spec, k)
+        if cpu and cpu.pop("total") != str(total):
+            raise AssertionError("GPU total differs from the reference")
+
+    if rank == 0:
+        line = {
+            "metric": f"k-cliques/s (k={k})", "value": value, "unit": "cliques/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 ids / u64 counts",
+            "data": "synthetic (in-repo deterministic generator, seeded)",
+            "config": config_obj(args.config, spec, k, g,
+                                 {"parallelism": f"sources r % {world}" if world > 1
+                                  else "single GPU"}),
+            "total": str(total),
+            "oriented_edges_per_s": g.m / (ms_per_step / 1e3),
+            "phases_ms": phase,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "count_stats": stats,
+            "secondary": secondary,
+        }
+        print(json.dumps(line))
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_kcg(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -56,6 +56,7 @@ typedef struct kcg_times {
   double download_ms; /* D2H of the last call's host outputs */
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
+  uint64_t launches;  /* kernels of this library launched on the handle, cumulative */
 } kcg_times;
 
 /* Static description of the counting work of the last kcg_count. */
@@ -120,6 +121,12 @@ int kcg_direct(kcg_graph* g, uint64_t* out_offsets, uint32_t* out_targets,
  * NULL for totals only, else n entries indexed by vertex id.
  * KCG_EINVAL for k < 2. */
 int kcg_count(kcg_graph* g, int k, uint64_t* total, uint64_t* per_vertex);
+/* Multi-GPU sharding: counts only the cliques whose
+ * lowest-ranked vertex r satisfies r % nparts == part.  Summing the
+ * totals (and per-vertex arrays) of all parts gives kcg_count's result;
+ * callers all-reduce them across GPUs.  per_vertex is NULL or n entries. */
+int kcg_count_part(kcg_graph* g, int k, uint32_t part, uint32_t nparts,
+                   uint64_t* total, uint64_t* per_vertex);
 /* Device pointer to the per-vertex counts of the last per-vertex count
  * (n u64, vertex-id order); valid until the next call on the handle. */
 int kcg_per_vertex_device(kcg_graph* g, const uint64_t** d_per_vertex);
@@ -133,6 +140,9 @@ int kcg_timings(const kcg_graph* g, kcg_times* out);
 int kcg_last_count_stats(const kcg_graph* g, kcg_count_stats* out);
 /* Bytes of device memory the handle currently holds. */
 uint64_t kcg_device_bytes(const kcg_graph* g);
+/* The CUDA stream (cudaStream_t) all of the handle's work is queued on,
+ * for callers that time or order work around it with CUDA events. */
+void* kcg_stream(kcg_graph* g);
 /* Blocks until all work queued on the handle's stream is done. */
 int kcg_synchronize(kcg_graph* g);
 

@@ -157,7 +157,7 @@ void finish_und(Graph& g) {
   g.deg.ensure(g.n, &g.bytes);
   if (g.n)
     degree_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.und_off.p, g.n, g.deg.p);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   g.has_und = true;
 }
 
@@ -171,7 +171,7 @@ void install_rank_device(Graph& g) {
   if (g.n)
     bijection_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.rank.p, g.n, seen,
                                                                    g.order.p, g.counters.p);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   unsigned long long bad = 0;
   KCG_CUDA(cudaMemcpyAsync(&bad, g.counters.p, 8, cudaMemcpyDeviceToHost, g.stream));
   g.sync();
@@ -385,6 +385,32 @@ int kcg_count(kcg_graph* h, int k, uint64_t* total, uint64_t* per_vertex) {
     }
     if (total) *total = t;
   });
+}
+
+int kcg_count_part(kcg_graph* h, int k, uint32_t part, uint32_t nparts, uint64_t* total,
+                   uint64_t* per_vertex) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (!g.has_rdag) {
+      if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
+      build_dag(g, false);
+    }
+    g.times.d2h_bytes = 0;
+    uint64_t t = count_cliques(g, k, per_vertex != nullptr, part, nparts);
+    if (per_vertex) {
+      g.mark(4);
+      download(g, per_vertex, g.pv.p, size_t(g.n) * 8);
+      g.mark(5);
+      g.sync();
+      g.times.download_ms = g.elapsed(4, 5);
+    }
+    if (total) *total = t;
+  });
+}
+
+void* kcg_stream(kcg_graph* h) {
+  return h ? static_cast<void*>(reinterpret_cast<Graph*>(h)->stream) : nullptr;
 }
 
 int kcg_per_vertex_device(kcg_graph* h, const uint64_t** d_per_vertex) {

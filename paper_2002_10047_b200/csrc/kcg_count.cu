@@ -659,13 +659,14 @@ __global__ void __launch_bounds__(CTA_THREADS) count_cta_kernel(CtaArgs a) {
 // Splits sources with d >= dmin into the warp tier list and the CTA/heavy
 // candidate list (key = d for sorting).
 __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, uint32_t dmin,
+                                uint32_t part, uint32_t nparts,
                                 uint32_t* __restrict__ wlist, uint32_t* __restrict__ clist,
                                 uint32_t* __restrict__ ckey, unsigned* __restrict__ cnt) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const uint32_t r = base + threadIdx.x;
     uint32_t d = 0;
-    if (r < n) d = uint32_t(off[r + 1] - off[r]);
+    if (r < n && r % nparts == part) d = uint32_t(off[r + 1] - off[r]);
     const bool inw = r < n && d >= dmin && d <= 32;
     const bool inc = r < n && d >= dmin && d > 32;
     unsigned bw = __ballot_sync(FULL, inw), bc = __ballot_sync(FULL, inc);
@@ -686,9 +687,10 @@ __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, ui
 }
 
 __global__ void k2_pv_kernel(const uint64_t* __restrict__ rdag_off,
-                             const uint32_t* __restrict__ rdag_adj, uint32_t n,
-                             ull* __restrict__ pv_rank) {
+                             const uint32_t* __restrict__ rdag_adj, uint32_t n, uint32_t part,
+                             uint32_t nparts, ull* __restrict__ pv_rank) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (r % nparts != part) continue;
     const uint64_t b = rdag_off[r], e = rdag_off[r + 1];
     if (e > b) atomicAdd(&pv_rank[r], ull(e - b));
     for (uint64_t p = b; p < e; p++) atomicAdd(&pv_rank[rdag_adj[p]], 1ull);
@@ -729,7 +731,7 @@ void launch_cta(Graph& g, CtaArgs a, uint32_t nsrc, bool global_ws, size_t heavy
     a.global_ws = 1;
   }
   count_cta_kernel<PV><<<grid, CTA_THREADS, smem, g.stream>>>(a);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   g.stats.launches++;
 }
 
@@ -737,7 +739,8 @@ inline ull* PVR(Graph& g) { return reinterpret_cast<ull*>(g.pv_rank.p); }
 
 }  // namespace
 
-uint64_t count_cliques(Graph& g, int k, bool want_pv) {
+uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t nparts) {
+  if (nparts == 0 || part >= nparts) fail(KCG_EINVAL, "part must be < nparts");
   if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
   if (!g.has_rdag) fail(KCG_EINVAL, "no DAG on the handle");
   const uint32_t n = g.n;
@@ -754,11 +757,18 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv) {
   uint64_t total = 0;
   if (k == 2) {
     // counting.cpp:165-173: every directed edge is a 2-clique
-    total = g.m;
+    total = nparts == 1 ? g.m : 0;
+    if (nparts > 1) {
+      std::vector<uint64_t> ro(size_t(n) + 1);
+      KCG_CUDA(cudaMemcpyAsync(ro.data(), g.rdag_off.p, ro.size() * 8, cudaMemcpyDeviceToHost,
+                               g.stream));
+      g.sync();
+      for (uint32_t r = part; r < n; r += nparts) total += ro[r + 1] - ro[r];
+    }
     if (want_pv && n) {
       k2_pv_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, n,
-                                                            PVR(g));
-      KCG_LAUNCH_CHECK();
+                                                            part, nparts, PVR(g));
+      KCG_LAUNCHED(g);
     }
     g.mark(6);
     g.mark(7);
@@ -773,9 +783,9 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv) {
     uint32_t* clist2 = reinterpret_cast<uint32_t*>(sb + 3 * nb);
     uint32_t* ckey2 = reinterpret_cast<uint32_t*>(sb + 4 * nb);
     unsigned* cnt = reinterpret_cast<unsigned*>(ctr + 2);
-    classify_kernel<<<blocks_for(n, 256, 148u * 16u), 256, 0, g.stream>>>(g.rdag_off.p, n, dmin,
-                                                                         wlist, clist, ckey, cnt);
-    KCG_LAUNCH_CHECK();
+    classify_kernel<<<blocks_for(n, 256, 148u * 16u), 256, 0, g.stream>>>(
+        g.rdag_off.p, n, dmin, part, nparts, wlist, clist, ckey, cnt);
+    KCG_LAUNCHED(g);
     unsigned hc[2] = {0, 0};
     KCG_CUDA(cudaMemcpyAsync(hc, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
     g.sync();
@@ -806,7 +816,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv) {
       else
         count_warp_kernel<false><<<grid, WARP_THREADS_BLOCK, 0, g.stream>>>(
             g.rdag_off.p, g.rdag_adj.p, wlist, nw, k, ctr, PVR(g), ctr + 1);
-      KCG_LAUNCH_CHECK();
+      KCG_LAUNCHED(g);
       g.stats.launches++;
     }
     g.stats.sources_warp = nw;
@@ -866,7 +876,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv) {
   if (want_pv && n) {
     gather_pv_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(PVR(g), g.rank.p, n,
                                                               reinterpret_cast<ull*>(g.pv.p));
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
   }
   ull hv[2] = {0, 0};
   KCG_CUDA(cudaMemcpyAsync(hv, ctr, 16, cudaMemcpyDeviceToHost, g.stream));

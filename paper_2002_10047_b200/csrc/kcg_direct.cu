@@ -152,7 +152,7 @@ void build_dag(Graph& g, bool want_id_dag) {
   unsigned grid = blocks_for(uint64_t(n) * 32, kThreads, 148u * 64u);
   if (n) outdeg_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n,
                                                         odeg, rdeg);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   exclusive_scan_u64(g, rdeg, g.rdag_off.p, size_t(n) + 1);
   if (odeg) exclusive_scan_u64(g, odeg, g.dag_off.p, size_t(n) + 1);
   if (n)
@@ -160,7 +160,7 @@ void build_dag(Graph& g, bool want_id_dag) {
                                                  want_id_dag ? g.dag_off.p : nullptr,
                                                  want_id_dag ? g.dag_adj.p : nullptr,
                                                  g.rdag_off.p, g.rdag_adj.p);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   sort_rdag_and_max(g, rdeg);
   g.mark(3);
   g.times.direct_ms = g.elapsed(2, 3);
@@ -178,14 +178,14 @@ void relabel_from_dag(Graph& g) {
   if (n)
     dag_deg_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(g.dag_off.p, g.rank.p, n,
                                                                        rdeg);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   exclusive_scan_u64(g, rdeg, g.rdag_off.p, size_t(n) + 1);
   unsigned long long* bad = g.counters.ensure(4, &g.bytes) + 2;
   KCG_CUDA(cudaMemsetAsync(bad, 0, 8, g.stream));
   if (n)
     relabel_kernel<<<blocks_for(uint64_t(n) * 32, kThreads, 148u * 64u), kThreads, 0, g.stream>>>(
         g.dag_off.p, g.dag_adj.p, g.rank.p, n, g.rdag_off.p, g.rdag_adj.p, bad);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   unsigned long long nbad = 0;
   KCG_CUDA(cudaMemcpyAsync(&nbad, bad, 8, cudaMemcpyDeviceToHost, g.stream));
   sort_rdag_and_max(g, rdeg);

@@ -33,6 +33,12 @@ void set_last_error(const std::string& msg);
     }                                                                        \
   } while (0)
 #define KCG_LAUNCH_CHECK() KCG_CUDA(cudaGetLastError())
+// after every kernel of this library: error check + launch accounting
+#define KCG_LAUNCHED(g)   \
+  do {                    \
+    KCG_LAUNCH_CHECK();   \
+    (g).times.launches++; \
+  } while (0)
 
 // ---- device buffers ----------------------------------------------------------
 template <class T>
@@ -145,7 +151,8 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
                     uint64_t* alpha_out);  // returns rounds
 void build_dag(Graph& g, bool want_id_dag);
 void relabel_from_dag(Graph& g);  // rdag from an adopted id-space DAG
-uint64_t count_cliques(Graph& g, int k, bool want_pv);
+uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part = 0,
+                       uint32_t nparts = 1);
 
 // small helpers
 void* cub_temp(Graph& g, size_t bytes);

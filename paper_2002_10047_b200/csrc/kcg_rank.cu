@@ -263,7 +263,7 @@ Peel peel_state(Graph& g, bool with_keys) {
     KCG_CUDA(cudaMemcpyAsync(p.wdeg, g.deg.p, n * 4, cudaMemcpyDeviceToDevice, g.stream));
     KCG_CUDA(cudaMemsetAsync(p.alive, 1, n, g.stream));
     iota_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(p.rem, uint32_t(n));
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
   }
   return p;
 }
@@ -301,7 +301,7 @@ void rank_degree(Graph& g) {
   uint32_t* keys_out = reinterpret_cast<uint32_t*>(base + off_vals);
   uint32_t* maxd = reinterpret_cast<uint32_t*>(base + 2 * off_vals);
   iota_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(vals_in, n);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
   size_t tb = 0;
   KCG_CUDA(cub::DeviceReduce::Max(nullptr, tb, g.deg.p, maxd, n, g.stream));
   KCG_CUDA(cub::DeviceReduce::Max(cub_temp(g, tb), tb, g.deg.p, maxd, n, g.stream));
@@ -317,7 +317,7 @@ void rank_degree(Graph& g) {
                                            g.order.p, n, 0, end_bit, g.stream));
   scatter_rank_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(g.order.p, n, 0,
                                                                           g.rank.p);
-  KCG_LAUNCH_CHECK();
+  KCG_LAUNCHED(g);
 }
 
 uint64_t rank_be(Graph& g, double eps, uint64_t alpha_hat) {
@@ -339,10 +339,10 @@ uint64_t rank_be(Graph& g, double eps, uint64_t alpha_hat) {
     }
     split_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(
         flag, P.rem, nrem, P.pos, P.batch, P.rem2, P.alive, 0, g.rank.p, placed);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     decrement_kernel<<<blocks_for(uint64_t(nb) * 32, kThreads), kThreads, 0, g.stream>>>(
         P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     std::swap(P.rem, P.rem2);
     nrem -= nb;
     placed += nb;
@@ -366,7 +366,7 @@ uint64_t rank_gp(Graph& g, double eps) {
     take = std::min<uint64_t>(take, nrem);
     gp_keys_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(P.rem, nrem, P.wdeg,
                                                                          idbits, P.keys);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     size_t tb = 0;
     int end_bit = std::min(64, idbits + 32);
     KCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, P.keys, P.keys2, nrem, 0, end_bit,
@@ -375,10 +375,10 @@ uint64_t rank_gp(Graph& g, double eps) {
                                             end_bit, g.stream));
     gp_take_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(
         P.keys2, nrem, uint32_t(take), idmask, placed, P.batch, P.rem2, P.alive, g.rank.p);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     decrement_kernel<<<blocks_for(take * 32, kThreads), kThreads, 0, g.stream>>>(
         P.batch, uint32_t(take), g.und_off.p, g.und_adj.p, P.alive, P.wdeg);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     std::swap(P.rem, P.rem2);
     nrem -= uint32_t(take);
     placed += uint32_t(take);
@@ -454,11 +454,11 @@ uint64_t rank_kcore(Graph& g) {
       }
       kcore_kill_rank_kernel<<<blocks_for(nf, kThreads), kThreads, 0, g.stream>>>(
           f, nf, placed, P.alive, g.rank.p);
-      KCG_LAUNCH_CHECK();
+      KCG_LAUNCHED(g);
       KCG_CUDA(cudaMemsetAsync(ctr, 0, 8, g.stream));
       kcore_decrement_kernel<<<blocks_for(uint64_t(nf) * 32, kThreads), kThreads, 0, g.stream>>>(
           f, nf, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, level, next, ctr);
-      KCG_LAUNCH_CHECK();
+      KCG_LAUNCHED(g);
       placed += nf;
       unsigned long long nn = 0;
       KCG_CUDA(cudaMemcpyAsync(&nn, ctr, 8, cudaMemcpyDeviceToHost, g.stream));
@@ -491,13 +491,13 @@ uint64_t estimate_impl(Graph& g, double eps) {
     if (nb == 0) fail(KCG_ERUNTIME, "arboricity estimate: empty batch");
     split_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(
         flag, P.rem, nrem, P.pos, P.batch, P.rem2, P.alive, 2, nullptr, 0);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     KCG_CUDA(cudaMemsetAsync(P.ctr, 0, 8, g.stream));
     arb_decrement_kernel<<<blocks_for(uint64_t(nb) * 32, kThreads), kThreads, 0, g.stream>>>(
         P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, P.ctr);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     kill_kernel<<<blocks_for(nb, kThreads), kThreads, 0, g.stream>>>(P.batch, nb, P.alive);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
     unsigned long long removed = 0;
     KCG_CUDA(cudaMemcpyAsync(&removed, P.ctr, 8, cudaMemcpyDeviceToHost, g.stream));
     g.sync();
@@ -532,7 +532,7 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
       break;
     case KCG_ORIGINAL:
       if (g.n) iota_kernel<<<blocks_for(g.n, kThreads), kThreads, 0, g.stream>>>(g.rank.p, g.n);
-      KCG_LAUNCH_CHECK();
+      KCG_LAUNCHED(g);
       break;
     case KCG_KCORE:
       rounds = rank_kcore(g);
@@ -551,7 +551,7 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
   g.order.ensure(g.n, &g.bytes);
   if (g.n && strategy != KCG_DEGREE) {
     invert_kernel<<<blocks_for(g.n, kThreads), kThreads, 0, g.stream>>>(g.rank.p, g.n, g.order.p);
-    KCG_LAUNCH_CHECK();
+    KCG_LAUNCHED(g);
   }
   g.mark(3);
   g.sync();

@@ -30,7 +30,8 @@ EXPORTED = [
     "kcg_graph_create_device", "kcg_dag_create", "kcg_graph_destroy", "kcg_num_vertices",
     "kcg_num_edges", "kcg_rank", "kcg_estimate_arboricity", "kcg_set_ranking", "kcg_direct",
     "kcg_count", "kcg_per_vertex_device", "kcg_pipeline", "kcg_timings",
-    "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize",
+    "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
+    "kcg_stream",
 ]
 
 
@@ -48,7 +49,8 @@ class Times(ctypes.Structure):
     _fields_ = [("upload_ms", ctypes.c_double), ("rank_ms", ctypes.c_double),
                 ("direct_ms", ctypes.c_double), ("count_ms", ctypes.c_double),
                 ("count_kernel_ms", ctypes.c_double), ("download_ms", ctypes.c_double),
-                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64)]
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64),
+                ("launches", ctypes.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -98,6 +100,9 @@ def lib():
         L.kcg_direct.argtypes = [vp, vp, vp, P(u64)]
         L.kcg_count.argtypes = [vp, ctypes.c_int, P(u64), vp]
         L.kcg_per_vertex_device.argtypes = [vp, P(vp)]
+        L.kcg_count_part.argtypes = [vp, ctypes.c_int, u32, u32, P(u64), vp]
+        L.kcg_stream.argtypes = [vp]
+        L.kcg_stream.restype = vp
         L.kcg_pipeline.argtypes = [vp, ctypes.c_int, ctypes.c_double, u64, ctypes.c_int,
                                    P(u64), vp]
         L.kcg_timings.argtypes = [vp, P(Times)]
@@ -146,6 +151,14 @@ class DeviceGraph:
         off, a = _u64(offsets), _u32(adj)
         h = ctypes.c_void_p()
         _check(lib().kcg_graph_create(len(off) - 1, off.ctypes.data, a.ctypes.data,
+                                      ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_csr_ptr(cls, n: int, offsets_ptr: int, adj_ptr: int) -> "DeviceGraph":
+        """Host pointers (e.g. pinned buffers) to offsets[n+1] u64, adj[2m] u32."""
+        h = ctypes.c_void_p()
+        _check(lib().kcg_graph_create(n, ctypes.c_void_p(offsets_ptr), ctypes.c_void_p(adj_ptr),
                                       ctypes.byref(h)))
         return cls(h)
 
@@ -221,6 +234,17 @@ class DeviceGraph:
         _check(lib().kcg_count(self._h, int(k), ctypes.byref(total),
                                pv.ctypes.data if per_vertex else None))
         return int(total.value), (pv[:self.n] if per_vertex else None)
+
+    def count_part(self, k: int, part: int, nparts: int, per_vertex=False):
+        """Cliques whose lowest-ranked vertex r has r % nparts == part."""
+        total = ctypes.c_uint64(0)
+        pv = np.zeros(max(self.n, 1), np.uint64) if per_vertex else None
+        _check(lib().kcg_count_part(self._h, int(k), int(part), int(nparts), ctypes.byref(total),
+                                    pv.ctypes.data if per_vertex else None))
+        return int(total.value), (pv[:self.n] if per_vertex else None)
+
+    def stream_ptr(self) -> int:
+        return int(lib().kcg_stream(self._h) or 0)
 
     def pipeline(self, strategy, eps, k, alpha_hat=0, per_vertex=False):
         if isinstance(strategy, str):
