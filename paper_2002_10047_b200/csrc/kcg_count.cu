@@ -52,134 +52,219 @@ constexpr uint32_t SMEM_TIER_MAX = 1024;  // largest d staged in shared memory
 __device__ __forceinline__ uint32_t above_mask(uint32_t b) {  // bits > b, b in [0,31]
   return b >= 31 ? 0u : (FULL << (b + 1));
 }
-__device__ __forceinline__ uint32_t hash_slot(uint32_t key, int bits) {
-  return (key * 0x9E3779B1u) >> (32 - bits);
-}
 __device__ __forceinline__ ull warp_sum(ull v) {
   for (int s = 16; s; s >>= 1) v += __shfl_xor_sync(FULL, v, s);
   return v;
 }
 
 // ---------------------------------------------------------------------------
-// Per-lane recursion over <= 32-vertex compact subproblems.
-// sym[x] = neighbours of x inside the subproblem (both directions); since
-// b only holds bits above the chosen x, b & sym[x] = (remaining) ∩ N+(x).
-// With PV, cpv[x] accumulates the number of counted cliques containing x
-// (excluding the caller's chain).
+// Staging: membership test for N+(u) and the flattened scan of its rows.
 // ---------------------------------------------------------------------------
-template <int R, bool PV>
-__device__ __forceinline__ ull lane_cnt(uint32_t J, const uint32_t* sym, ull* cpv) {
-  if constexpr (R == 1) {
-    if constexpr (PV) {
-      for (uint32_t b = J; b; b &= b - 1) atomicAdd(&cpv[__ffs(b) - 1], 1ull);
-    }
-    return __popc(J);
-  } else if constexpr (R == 2) {
-    ull t = 0;
-    for (uint32_t b = J; b;) {
-      int x = __ffs(b) - 1;
-      b &= b - 1;
-      uint32_t sx = sym[x];
-      t += __popc(b & sx);
-      if constexpr (PV) {
-        uint32_t c = __popc(J & sx);
-        if (c) atomicAdd(&cpv[x], ull(c));
+constexpr ull EMPTY64 = ~0ull;
+
+// Open-addressing table of (key | local index << 32) plus a 1-bit-per-slot
+// filter; most probes of a scan miss and cost one shared load of the
+// filter word.
+struct Member {
+  ull* table;
+  uint32_t* filter;
+  uint32_t tbits, fbits;
+};
+
+__device__ __forceinline__ void member_insert(const Member& M, uint32_t key, uint32_t idx) {
+  const uint32_t h = key * 0x9E3779B1u;
+  const uint32_t fb = h >> (32 - M.fbits);
+  atomicOr(&M.filter[fb >> 5], 1u << (fb & 31));
+  const uint32_t mask = (1u << M.tbits) - 1;
+  uint32_t slot = h >> (32 - M.tbits);
+  const ull packed = ull(key) | (ull(idx) << 32);
+  while (atomicCAS(&M.table[slot], EMPTY64, packed) != EMPTY64) slot = (slot + 1) & mask;
+}
+
+__device__ __forceinline__ uint32_t member_find(const Member& M, uint32_t key) {
+  const uint32_t h = key * 0x9E3779B1u;
+  const uint32_t fb = h >> (32 - M.fbits);
+  if (!((M.filter[fb >> 5] >> (fb & 31)) & 1u)) return NOTFOUND;
+  const uint32_t mask = (1u << M.tbits) - 1;
+  uint32_t slot = h >> (32 - M.tbits);
+  for (;;) {
+    const ull e = M.table[slot];
+    if (uint32_t(e) == key) return uint32_t(e >> 32);
+    if (uint32_t(e) == EMPTY) return NOTFOUND;
+    slot = (slot + 1) & mask;
+  }
+}
+
+// Non-empty rows of a source in local order: row r is N+(w_rowid[r]),
+// global elements adj[rbase[r] ..), first virtual position P[r]; P[nr] = L.
+struct Rows {
+  const uint32_t* P;
+  const ull* rbase;
+  const uint32_t* rowid;
+  uint32_t nr;
+};
+
+// One warp stages virtual positions [pbeg, pend) of the concatenated rows:
+// 32 consecutive elements per chunk, one per lane; a lane finds its row
+// from the bitmask of row starts inside the chunk (one REDUX.OR); STAGE_U
+// chunks issue their global loads before any lookup so several loads per
+// lane are in flight.  Every hit j in row i sets sym(i, j) and sym(j, i).
+constexpr int STAGE_U = 4;
+
+__device__ __forceinline__ void stage_range(const Rows& R, const Member& M,
+                                            const uint32_t* __restrict__ adj, uint32_t* sym,
+                                            uint32_t wp, uint32_t pbeg, uint32_t pend,
+                                            uint32_t lane) {
+  if (pbeg >= pend) return;
+  uint32_t lo = 0, hi = R.nr;  // P[lo] <= pbeg < P[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (R.P[mid] <= pbeg)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  uint32_t cur = lo, pcur = R.P[lo];
+  const uint32_t le_mask = (2u << lane) - 1u;
+  for (uint32_t c0 = pbeg; c0 < pend; c0 += 32 * STAGE_U) {
+    // reconverge after the previous chunk's data-dependent probe loops so
+    // the REDUX/VOTE/SHFL below take the converged fast path
+    __syncwarp();
+    uint32_t y[STAGE_U], row[STAGE_U];
+#pragma unroll
+    for (int u = 0; u < STAGE_U; u++) {
+      const uint32_t cb = c0 + 32 * u;
+      const uint32_t p = cb + lane;
+      const uint32_t jn = cur + 1 + lane;
+      const uint32_t pn = jn <= R.nr ? R.P[jn] : 0xffffffffu;
+      const uint32_t rel = pn - cb;
+      const uint32_t starts = __reduce_or_sync(FULL, rel < 32u ? (1u << rel) : 0u);
+      const uint32_t kk = __popc(starts & le_mask);
+      const uint32_t seg = cur + kk;
+      uint32_t pseg = __shfl_sync(FULL, pn, (kk - 1) & 31);
+      if (kk == 0) pseg = pcur;
+      const uint32_t adv = __popc(__ballot_sync(FULL, pn <= cb + 32));
+      const uint32_t pnext = __shfl_sync(FULL, pn, (adv - 1) & 31);
+      if (adv) pcur = pnext;
+      cur += adv;
+      y[u] = EMPTY;
+      row[u] = 0;
+      if (p < pend) {
+        y[u] = __ldg(adj + R.rbase[seg] + (p - pseg));
+        row[u] = R.rowid[seg];
       }
     }
-    return t;
-  } else {
-    ull t = 0;
-    for (uint32_t b = J; b;) {
-      int x = __ffs(b) - 1;
-      b &= b - 1;
-      if (__popc(b) < R - 1) break;
-      uint32_t J2 = b & sym[x];
-      if (__popc(J2) >= R - 1) {
-        ull c = lane_cnt<R - 1, PV>(J2, sym, cpv);
-        t += c;
-        if constexpr (PV) {
-          if (c) atomicAdd(&cpv[x], c);
+#pragma unroll
+    for (int u = 0; u < STAGE_U; u++) {
+      if (y[u] != EMPTY) {
+        const uint32_t j = member_find(M, y[u]);
+        if (j != NOTFOUND) {
+          const uint32_t i = row[u];
+          atomicOr(&sym[size_t(i) * wp + (j >> 5)], 1u << (j & 31));
+          atomicOr(&sym[size_t(j) * wp + (i >> 5)], 1u << (i & 31));
         }
       }
     }
-    return t;
   }
 }
 
-// Explicit-stack variant for R beyond the templated depths.
-template <bool PV>
-__device__ __noinline__ ull lane_cnt_generic(uint32_t J, int R, const uint32_t* sym, ull* cpv) {
-  uint32_t S[33];
-  int X[33];
-  ull C[33];
-  int lvl = 0;
-  S[0] = J;
-  C[0] = 0;
-  for (;;) {
-    uint32_t b = S[lvl];
-    const int rr = R - lvl;
-    if (__popc(b) < rr) {
-      if (lvl == 0) break;
-      ull c = C[lvl];
-      lvl--;
-      C[lvl] += c;
-      if (PV && c) atomicAdd(&cpv[X[lvl]], c);
-      continue;
+// Rows of >= 32 elements: a 32-element chunk touches at most two rows, so a
+// lane's row is one compare against the warp-uniform boundary pnext.
+__device__ __forceinline__ void stage_long(const Rows& R, const Member& M,
+                                           const uint32_t* __restrict__ adj, uint32_t* sym,
+                                           uint32_t wp, uint32_t pbeg, uint32_t pend,
+                                           uint32_t lane) {
+  if (pbeg >= pend) return;
+  uint32_t lo = 0, hi = R.nr;  // P[lo] <= pbeg < P[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (R.P[mid] <= pbeg)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  uint32_t cur = lo;
+  uint32_t pnext = R.P[cur + 1];
+  ull bcur = R.rbase[cur] - R.P[cur];
+  uint32_t rcur = R.rowid[cur];
+  ull bnxt = 0;
+  uint32_t rnxt = 0;
+  if (cur + 1 < R.nr) {
+    bnxt = R.rbase[cur + 1] - pnext;
+    rnxt = R.rowid[cur + 1];
+  }
+  for (uint32_t c0 = pbeg; c0 < pend; c0 += 32 * STAGE_U) {
+    uint32_t y[STAGE_U], row[STAGE_U];
+#pragma unroll
+    for (int u = 0; u < STAGE_U; u++) {
+      const uint32_t cb = c0 + 32 * u;
+      const uint32_t p = cb + lane;
+      const bool nx = p >= pnext;
+      y[u] = EMPTY;
+      row[u] = nx ? rnxt : rcur;
+      if (p < pend) y[u] = __ldg(adj + (nx ? bnxt : bcur) + p);
+      if (cb + 32 >= pnext && cb + 32 < pend) {  // warp-uniform row advance
+        cur++;
+        bcur = bnxt;
+        rcur = rnxt;
+        pnext = R.P[cur + 1];
+        if (cur + 1 < R.nr) {
+          bnxt = R.rbase[cur + 1] - pnext;
+          rnxt = R.rowid[cur + 1];
+        }
+      }
     }
-    int x = __ffs(b) - 1;
-    b &= b - 1;
-    S[lvl] = b;
-    uint32_t J2 = b & sym[x];
-    const int r2 = rr - 1;
-    if (__popc(J2) < r2) continue;
-    if (r2 == 2) {
-      ull c = lane_cnt<2, PV>(J2, sym, cpv);
-      C[lvl] += c;
-      if (PV && c) atomicAdd(&cpv[x], c);
-    } else {
-      X[lvl] = x;
-      lvl++;
-      S[lvl] = J2;
-      C[lvl] = 0;
+#pragma unroll
+    for (int u = 0; u < STAGE_U; u++) {
+      if (y[u] != EMPTY) {
+        const uint32_t j = member_find(M, y[u]);
+        if (j != NOTFOUND) {
+          const uint32_t i = row[u];
+          atomicOr(&sym[size_t(i) * wp + (j >> 5)], 1u << (j & 31));
+          atomicOr(&sym[size_t(j) * wp + (i >> 5)], 1u << (i & 31));
+        }
+      }
     }
   }
-  return C[0];
 }
 
-template <bool PV>
-__device__ ull lane_count(uint32_t J, int R, const uint32_t* sym, ull* cpv) {
-  if (__popc(J) < R) return 0;
-  switch (R) {
-    case 1: return lane_cnt<1, PV>(J, sym, cpv);
-    case 2: return lane_cnt<2, PV>(J, sym, cpv);
-    case 3: return lane_cnt<3, PV>(J, sym, cpv);
-    case 4: return lane_cnt<4, PV>(J, sym, cpv);
-    case 5: return lane_cnt<5, PV>(J, sym, cpv);
-    case 6: return lane_cnt<6, PV>(J, sym, cpv);
-    case 7: return lane_cnt<7, PV>(J, sym, cpv);
-    case 8: return lane_cnt<8, PV>(J, sym, cpv);
-    default: return lane_cnt_generic<PV>(J, R, sym, cpv);
-  }
-}
+}  // namespace
+}  // namespace kcg
+
+#include "kcg_dfs.cuh"
+
+namespace kcg {
+namespace {
 
 // ---------------------------------------------------------------------------
 // Warp tier: one warp per source u with 2 <= d <= 32.
 // ---------------------------------------------------------------------------
-template <bool PV>
+template <bool PV, int MAXL>
 __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     count_warp_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                       const uint32_t* __restrict__ srcs, uint32_t nsrc, int k,
                       ull* __restrict__ total_out, ull* __restrict__ pv_rank,
                       ull* __restrict__ staged_out) {
-  __shared__ uint32_t s_sym[WARP_TIER_WARPS][32];
-  __shared__ uint32_t s_key[WARP_TIER_WARPS][64];
-  __shared__ uint8_t s_idx[WARP_TIER_WARPS][64];
+  struct WarpSmem {
+    ull table[64];
+    ull rbase[32];
+    uint32_t sym[32];
+    uint32_t usym[32];
+    uint32_t P[34];
+    uint32_t rowid[32];
+    uint32_t filter[16];
+    uint32_t map[32];
+  };
+  __shared__ WarpSmem s_w[WARP_TIER_WARPS];
   __shared__ ull s_pv[PV ? WARP_TIER_WARPS : 1][32];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];  // per-warp DFS stacks
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint32_t* sym = s_sym[wib];
-  uint32_t* hkey = s_key[wib];
-  uint8_t* hidx = s_idx[wib];
+  WarpSmem& S = s_w[wib];
+  constexpr int SL = MAXL > 0 ? MAXL : 1;
+  Stacks<PV, SL>* stk = reinterpret_cast<Stacks<PV, SL>*>(dyn_smem) + wib;
+  uint32_t* sym = S.sym;
   ull* cpv = s_pv[PV ? wib : 0];
+  const Member M{S.table, S.filter, 6, 9};
   const int R = k - 2;
   ull my_total = 0, my_staged = 0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -189,74 +274,78 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     const uint64_t b = off[u];
     const uint32_t d = uint32_t(off[u + 1] - b);
     const uint32_t w = lane < d ? adj[b + lane] : 0u;
-    hkey[lane] = EMPTY;
-    hkey[lane + 32] = EMPTY;
+    S.table[lane] = EMPTY64;
+    S.table[lane + 32] = EMPTY64;
+    if (lane < 16) S.filter[lane] = 0;
     sym[lane] = 0;
     if constexpr (PV) cpv[lane] = 0;
-    __syncwarp();
-    if (lane < d) {
-      uint32_t slot = hash_slot(w, 6);
-      while (atomicCAS(&hkey[slot], EMPTY, w) != EMPTY) slot = (slot + 1) & 63;
-      hidx[slot] = uint8_t(lane);
-    }
     uint64_t sb = 0;
     uint32_t len = 0;
     if (lane < d) {
       sb = off[w];
       len = uint32_t(off[w + 1] - sb);
     }
-    // inclusive scan of segment lengths
-    uint32_t incl = len;
+    __syncwarp();
+    if (lane < d) member_insert(M, w, lane);
+    // split the non-empty rows into long (>= 32) and short ones, each list
+    // compacted with its own prefix of lengths; long rows at [0, nl),
+    // short rows at [nl, nl + ns) with their prefix at P[nl + 1 ..]
+    const bool lg = len >= 32, sh = len > 0 && len < 32;
+    const unsigned ml = __ballot_sync(FULL, lg), ms = __ballot_sync(FULL, sh);
+    const uint32_t nl = __popc(ml), ns = __popc(ms);
+    uint32_t il = lg ? len : 0, is = sh ? len : 0;
     for (int s = 1; s < 32; s <<= 1) {
-      uint32_t t = __shfl_up_sync(FULL, incl, s);
-      if (lane >= uint32_t(s)) incl += t;
+      const uint32_t tl = __shfl_up_sync(FULL, il, s), ts = __shfl_up_sync(FULL, is, s);
+      if (lane >= uint32_t(s)) {
+        il += tl;
+        is += ts;
+      }
     }
-    const uint32_t excl = incl - len;
-    const uint32_t L = __shfl_sync(FULL, incl, 31);
+    const uint32_t Ll = __shfl_sync(FULL, il, 31), Ls = __shfl_sync(FULL, is, 31);
+    const unsigned below = (1u << lane) - 1;
+    if (lg) {
+      const uint32_t ci = __popc(ml & below);
+      S.P[ci] = il - len;
+      S.rbase[ci] = sb;
+      S.rowid[ci] = lane;
+    } else if (sh) {
+      const uint32_t ci = __popc(ms & below);
+      S.P[nl + 1 + ci] = is - len;
+      S.rbase[nl + ci] = sb;
+      S.rowid[nl + ci] = lane;
+    }
+    if (lane == 0) {
+      S.P[nl] = Ll;
+      S.P[nl + 1 + ns] = Ls;
+    }
     my_staged += len;
     __syncwarp();
-    // flattened scan of all out-lists N+(w_i): 32 consecutive entries per
-    // step, each lane finds its segment by a 5-step shuffle search
-    for (uint32_t c0 = 0; c0 < L; c0 += 32) {
-      const uint32_t p = c0 + lane;
-      uint32_t seg = 0;
-#pragma unroll
-      for (int step = 16; step; step >>= 1) {
-        uint32_t cand = seg + step;
-        uint32_t pe = __shfl_sync(FULL, excl, cand);
-        if (pe <= p && cand < d) seg = cand;
-      }
-      const uint64_t sbase = __shfl_sync(FULL, sb, seg);
-      const uint32_t sex = __shfl_sync(FULL, excl, seg);
-      if (p < L) {
-        const uint32_t y = adj[sbase + (p - sex)];
-        uint32_t slot = hash_slot(y, 6);
-        uint32_t j = NOTFOUND;
-        for (;;) {
-          uint32_t kk = hkey[slot];
-          if (kk == y) {
-            j = hidx[slot];
-            break;
-          }
-          if (kk == EMPTY) break;
-          slot = (slot + 1) & 63;
-        }
-        if (j != NOTFOUND) {
-          atomicOr(&sym[seg], 1u << j);
-          atomicOr(&sym[j], 1u << seg);
-        }
-      }
+    {
+      const Rows rl{S.P, S.rbase, S.rowid, nl};
+      stage_long(rl, M, adj, sym, 1, 0, Ll, lane);
+      const Rows rs{S.P + nl + 1, S.rbase + nl, S.rowid + nl, ns};
+      stage_range(rs, M, adj, sym, 1, 0, Ls, lane);
     }
     __syncwarp();
+    S.usym[lane] = sym[lane] & above_mask(lane);
+    __syncwarp();
     ull c = 0;
-    if (lane < d) {
-      uint32_t row = sym[lane] & above_mask(lane);
-      c = lane_count<PV>(row, R, sym, cpv);
-      my_total += c;
-      if constexpr (PV) {
-        if (c) atomicAdd(&cpv[lane], c);
+    if (R == 1) {
+      if (lane < d) {
+        c = __popc(S.usym[lane]);
+        if constexpr (PV) {
+          for (uint32_t bb = S.usym[lane]; bb; bb &= bb - 1) atomicAdd(&cpv[__ffs(bb) - 1], 1ull);
+          if (c) atomicAdd(&cpv[lane], c);
+        }
       }
+    } else if (R == 2) {
+      c = lane_pairs<PV>(lane < d, S.usym[lane], lane, S.usym, sym, cpv);
+    } else if (R <= 32) {
+      if constexpr (MAXL > 0)
+        c = steal_count<PV, SL>(lane < d, S.usym[lane], R, lane, S.usym, sym, cpv, *stk, S.map,
+                                lane);
     }
+    my_total += c;
     if constexpr (PV) {
       __syncwarp();
       ull src_total = warp_sum(c);
@@ -282,55 +371,69 @@ struct Lvl {
 
 // Byte layout of one CTA's working set (shared memory or a global slice).
 struct Layout {
-  uint32_t dmax, wpmax, tbits, levels;
-  size_t sym, hkey, hidx, pvl, warp0, warp_stride;
+  uint32_t dmax, wpmax, tbits, fbits, levels;
+  size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
   // per-warp offsets
-  size_t w_cand, w_stack, w_csym, w_cpv, w_lvl;
+  size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk;
   size_t total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bool pv) {
+__host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bool pv, int nw,
+                                              size_t stk_bytes) {
   Layout L;
   L.dmax = dmax;
   L.wpmax = ((dmax + 31) / 32) | 1u;
-  int tb = 6;
+  uint32_t tb = 6;
   while ((1u << tb) < 2 * dmax) tb++;
   L.tbits = tb;
+  L.fbits = tb + 4 > 14 ? (tb + 4 > 20 ? 20 : tb + 4) : 14;  // >= 8 filter bits per key
   L.levels = levels;
   size_t at = 0;
   L.sym = at;
   at = align_up(at + size_t(dmax) * L.wpmax * 4, 16);
-  L.hkey = at;
-  at = align_up(at + (size_t(1) << tb) * 4, 16);
-  L.hidx = at;
-  at = align_up(at + (size_t(1) << tb) * 2, 16);
+  L.table = at;
+  at = align_up(at + (size_t(1) << tb) * 8, 16);
+  L.filter = at;
+  at = align_up(at + (size_t(1) << L.fbits) / 8, 16);
+  L.rP = at;
+  at = align_up(at + (size_t(dmax) + 2) * 4, 16);
+  L.rbase = at;
+  at = align_up(at + size_t(dmax) * 8, 16);
+  L.rowid = at;
+  at = align_up(at + size_t(dmax) * 4, 16);
   L.pvl = at;
   at = align_up(at + (pv ? size_t(dmax) * 8 : 0), 16);
   L.warp0 = at;
   size_t w = 0;
   L.w_cand = w;
-  w = align_up(w + size_t(dmax) * 2 + 64, 16);
+  w = align_up(w + 32 * 4 + 128, 16);
   L.w_stack = w;
   w = align_up(w + size_t(levels) * L.wpmax * 4, 16);
   L.w_csym = w;
+  w = align_up(w + 32 * 4, 16);
+  L.w_cusym = w;
   w = align_up(w + 32 * 4, 16);
   L.w_cpv = w;
   w = align_up(w + (pv ? 32 * 8 : 0), 16);
   L.w_lvl = w;
   w = align_up(w + size_t(levels) * sizeof(Lvl), 16);
+  L.w_stk = w;
+  w = align_up(w + stk_bytes, 16);
   L.warp_stride = w;
-  L.total = align_up(at + w * CTA_WARPS, 128);
+  L.total = align_up(at + w * nw, 128);
   return L;
 }
 
 struct WarpCtx {
   const uint32_t* sym;  // CTA bitmap, row stride wp
   uint32_t wp, W;
-  uint16_t* cand;
+  uint32_t* cand;
   uint32_t* stack;      // levels x wp words
-  uint32_t* csym;       // 32 words
+  uint32_t* csym;       // 32 words: compact rows, both directions
+  uint32_t* cusym;      // 32 words: compact rows, upper part
+  void* stk;            // Stacks<PV, MAXL> of the warp's DFS engine
   ull* cpv;             // 32 (PV)
   ull* pvl;             // d (PV)
   Lvl* lvl;
@@ -364,7 +467,7 @@ __device__ uint32_t enumerate_members(const WarpCtx& c, const uint32_t* S, uint3
       if (c.lane >= uint32_t(s)) incl += t;
     }
     uint32_t pos = base + incl - n;
-    for (; v && pos < limit; v &= v - 1) c.cand[pos++] = uint16_t(32 * w + __ffs(v) - 1);
+    for (; v && pos < limit; v &= v - 1) c.cand[pos++] = 32 * w + __ffs(v) - 1;
     base += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
@@ -373,7 +476,7 @@ __device__ uint32_t enumerate_members(const WarpCtx& c, const uint32_t* S, uint3
 
 // |S| <= 32: transpose S's induced rows into one word per member (ballot),
 // then finish the remaining R-1 levels per lane.
-template <bool PV>
+template <bool PV, int MAXL>
 __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, int R) {
   enumerate_members(c, S, 32);
   const uint32_t lane = c.lane;
@@ -387,14 +490,19 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
     if (lane == r) mine = bal;
   }
   c.csym[lane] = mine;
+  c.cusym[lane] = mine & above_mask(lane);
   if constexpr (PV) c.cpv[lane] = 0;
   __syncwarp();
+  // R >= 3 here: every member t roots a (R-1)-clique search in its
+  // compact out-neighbourhood, balanced across lanes by the DFS engine
   ull ct = 0;
-  if (lane < s) {
-    ct = lane_count<PV>(mine & above_mask(lane), R - 1, c.csym, c.cpv);
-    if constexpr (PV) {
-      if (ct) atomicAdd(&c.cpv[lane], ct);
-    }
+  if constexpr (MAXL == 0) {
+    ct = lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv);  // R == 3
+  } else {
+    ct = R == 3 ? lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv)
+                : steal_count<PV, MAXL>(lane < s, c.cusym[lane], R - 1, lane, c.cusym, c.csym,
+                                        c.cpv, *reinterpret_cast<Stacks<PV, MAXL>*>(c.stk),
+                                        c.cand, lane);
   }
   __syncwarp();
   if constexpr (PV) {
@@ -405,28 +513,44 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
   return tot;
 }
 
-// R == 2 with |S| > 32: sum over members x of |S ∩ N+(x)|, one member per
-// lane, multi-word dot products.
+// R == 2: sum over members x of |S ∩ N+(x)|, one member per lane, each
+// lane running its member's multi-word dot product.  Members are gathered
+// 32 at a time into the warp's 32-entry candidate buffer.
 template <bool PV>
 __device__ ull dot_count(const WarpCtx& c, const uint32_t* S, uint32_t s) {
-  uint32_t ns = enumerate_members(c, S, 0xffffffffu);
   (void)s;
   ull cnt = 0;
-  for (uint32_t t = c.lane; t < ns; t += 32) {
-    const uint32_t x = c.cand[t];
-    const uint32_t* row = c.sym + size_t(x) * c.wp;
-    const uint32_t w0 = x >> 5;
-    uint32_t acc = __popc(S[w0] & row[w0] & above_mask(x & 31));
-    for (uint32_t w = w0 + 1; w < c.W; w++) acc += __popc(S[w] & row[w]);
-    cnt += acc;
-    if constexpr (PV) {
-      uint32_t all = __popc(S[w0] & row[w0] & ~above_mask(x & 31));
-      for (uint32_t w = 0; w < w0; w++) all += __popc(S[w] & row[w]);
-      all += acc;
-      if (all) atomicAdd(&c.pvl[x], ull(all));
+  for (uint32_t w0 = 0; w0 < c.W; w0 += 32) {
+    const uint32_t wl = w0 + c.lane;
+    uint32_t v = wl < c.W ? S[wl] : 0u;
+    while (__any_sync(FULL, v != 0)) {
+      const uint32_t n = __popc(v);
+      uint32_t incl = n;
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, sh);
+        if (c.lane >= uint32_t(sh)) incl += t;
+      }
+      const uint32_t tot = __shfl_sync(FULL, incl, 31);
+      for (uint32_t pos = incl - n; v && pos < 32; pos++, v &= v - 1)
+        c.cand[pos] = 32 * wl + __ffs(v) - 1;
+      __syncwarp();
+      if (c.lane < min(tot, 32u)) {
+        const uint32_t x = c.cand[c.lane];
+        const uint32_t* row = c.sym + size_t(x) * c.wp;
+        const uint32_t xw = x >> 5;
+        uint32_t acc = __popc(S[xw] & row[xw] & above_mask(x & 31));
+        for (uint32_t w = xw + 1; w < c.W; w++) acc += __popc(S[w] & row[w]);
+        cnt += acc;
+        if constexpr (PV) {
+          uint32_t all = __popc(S[xw] & row[xw] & ~above_mask(x & 31));
+          for (uint32_t w = 0; w < xw; w++) all += __popc(S[w] & row[w]);
+          all += acc;
+          if (all) atomicAdd(&c.pvl[x], ull(all));
+        }
+      }
+      __syncwarp();
     }
   }
-  __syncwarp();
   return warp_sum(cnt);
 }
 
@@ -449,13 +573,13 @@ __device__ uint32_t child_set(const WarpCtx& c, const uint32_t* S, uint32_t x, u
 }
 
 // count(S, R) for a set held in stack level 0 with |S| = s.
-template <bool PV>
+template <bool PV, int MAXL>
 __device__ ull warp_count(const WarpCtx& c, uint32_t s, int R) {
   const uint32_t* S0 = c.stack;
   if (uint32_t(R) > s) return 0;
   if (R == 1) return set_members_pv<PV>(c, S0);
-  if (s <= 32) return compact_count<PV>(c, S0, s, R);
   if (R == 2) return dot_count<PV>(c, S0, s);
+  if (s <= 32) return compact_count<PV, MAXL>(c, S0, s, R);
   // warp-cooperative DFS over sets larger than 32
   Lvl* st = c.lvl;
   int L = 0;
@@ -494,10 +618,10 @@ __device__ ull warp_count(const WarpCtx& c, uint32_t s, int R) {
     if (sc >= rc) {
       if (rc == 1) {
         add = set_members_pv<PV>(c, child);
-      } else if (sc <= 32) {
-        add = compact_count<PV>(c, child, sc, int(rc));
       } else if (rc == 2) {
         add = dot_count<PV>(c, child, sc);
+      } else if (sc <= 32) {
+        add = compact_count<PV, MAXL>(c, child, sc, int(rc));
       } else {
         descend = true;
       }
@@ -518,37 +642,52 @@ __device__ ull warp_count(const WarpCtx& c, uint32_t s, int R) {
 struct CtaArgs {
   const uint64_t* off;
   const uint32_t* adj;
-  const uint32_t* srcs;
-  uint32_t nsrc;
+  const uint32_t* item_src;  // source vertex (rank id) of each work item
+  const uint32_t* item_sl;   // (slice << 16) | nslices: the item counts
+                             // edges i with i % nslices == slice
+  uint32_t nitems;
   int k;
   ull* total;
   ull* pv_rank;
   ull* staged;
-  unsigned* work;        // source counter
-  unsigned* ework;       // per-CTA edge counters (global tier)
+  unsigned* work;        // work-item counter
   unsigned char* gbase;  // global working sets (heavy tier)
   Layout L;
-  int global_ws;
 };
 
-template <bool PV>
-__global__ void __launch_bounds__(CTA_THREADS) count_cta_kernel(CtaArgs a) {
+// GWS = false: the whole working set is dynamic shared memory (the
+// compiler sees shared-memory pointers and emits LDS/STS/ATOMS); true:
+// per-CTA slices of a global arena (heavy tier).
+template <bool PV, bool GWS, int NT, int MAXL>
+__global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_src, s_edge;
   __shared__ ull s_src_total;
+  typedef cub::BlockScan<ull, NT> BlockScanU64;
+  __shared__ typename BlockScanU64::TempStorage s_scan;
   const Layout& L = a.L;
-  unsigned char* base = a.global_ws ? a.gbase + size_t(blockIdx.x) * L.total : smem;
+  unsigned char* base;
+  if constexpr (GWS)
+    base = a.gbase + size_t(blockIdx.x) * L.total;
+  else
+    base = smem;
   uint32_t* sym = reinterpret_cast<uint32_t*>(base + L.sym);
-  uint32_t* hkey = reinterpret_cast<uint32_t*>(base + L.hkey);
-  uint16_t* hidx = reinterpret_cast<uint16_t*>(base + L.hidx);
+  ull* table = reinterpret_cast<ull*>(base + L.table);
+  uint32_t* filter = reinterpret_cast<uint32_t*>(base + L.filter);
+  uint32_t* rP = reinterpret_cast<uint32_t*>(base + L.rP);
+  ull* rbase = reinterpret_cast<ull*>(base + L.rbase);
+  uint32_t* rowid = reinterpret_cast<uint32_t*>(base + L.rowid);
   ull* pvl = reinterpret_cast<ull*>(base + L.pvl);
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* wbase = base + L.warp0 + size_t(wib) * L.warp_stride;
   WarpCtx c;
   c.sym = sym;
-  c.cand = reinterpret_cast<uint16_t*>(wbase + L.w_cand);
+  c.cand = reinterpret_cast<uint32_t*>(wbase + L.w_cand);
   c.stack = reinterpret_cast<uint32_t*>(wbase + L.w_stack);
   c.csym = reinterpret_cast<uint32_t*>(wbase + L.w_csym);
+  c.cusym = reinterpret_cast<uint32_t*>(wbase + L.w_cusym);
+  c.stk = wbase + L.w_stk;
   c.cpv = reinterpret_cast<ull*>(wbase + L.w_cpv);
   c.lvl = reinterpret_cast<Lvl*>(wbase + L.w_lvl);
   c.pvl = pvl;
@@ -563,57 +702,87 @@ __global__ void __launch_bounds__(CTA_THREADS) count_cta_kernel(CtaArgs a) {
     }
     __syncthreads();
     const uint32_t si = s_src;
-    if (si >= a.nsrc) break;
-    const uint32_t u = a.srcs[si];
+    if (si >= a.nitems) break;
+    const uint32_t u = a.item_src[si];
+    const uint32_t slice = a.item_sl[si] >> 16, nsl = a.item_sl[si] & 0xffffu;
     const uint64_t b = a.off[u];
     const uint32_t d = uint32_t(a.off[u + 1] - b);
     const uint32_t W = (d + 31) / 32, wp = W | 1u;
-    int tb = 6;
+    uint32_t tb = 6;
     while ((1u << tb) < 2 * d) tb++;
-    const uint32_t T = 1u << tb, tmask = T - 1;
+    const uint32_t fb = tb + 4 > 14 ? (tb + 4 > 20 ? 20 : tb + 4) : 14;
+    const Member M{table, filter, tb, fb};
     c.wp = wp;
     c.W = W;
-    for (uint32_t i = threadIdx.x; i < d * wp; i += CTA_THREADS) sym[i] = 0;
-    for (uint32_t i = threadIdx.x; i < T; i += CTA_THREADS) hkey[i] = EMPTY;
+    for (uint32_t i = threadIdx.x; i < d * wp; i += NT) sym[i] = 0;
+    for (uint32_t i = threadIdx.x; i < (1u << tb); i += NT) table[i] = EMPTY64;
+    for (uint32_t i = threadIdx.x; i < (1u << fb) / 32; i += NT) filter[i] = 0;
     if constexpr (PV) {
-      for (uint32_t i = threadIdx.x; i < d; i += CTA_THREADS) pvl[i] = 0;
+      for (uint32_t i = threadIdx.x; i < d; i += NT) pvl[i] = 0;
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < d; i += CTA_THREADS) {
-      uint32_t w = a.adj[b + i];
-      uint32_t slot = hash_slot(w, tb);
-      while (atomicCAS(&hkey[slot], EMPTY, w) != EMPTY) slot = (slot + 1) & tmask;
-      hidx[slot] = uint16_t(i);
-    }
-    __syncthreads();
-    // stage the induced subgraph: warp per row, lanes over N+(w_i)
-    for (uint32_t i = wib; i < d; i += CTA_WARPS) {
-      const uint32_t wi = a.adj[b + i];
-      const uint64_t rb = a.off[wi], re = a.off[wi + 1];
-      if (lane == 0) my_staged += re - rb;
-      for (uint64_t p = rb + lane; p < re; p += 32) {
-        const uint32_t y = a.adj[p];
-        uint32_t slot = hash_slot(y, tb);
-        for (;;) {
-          uint32_t kk = hkey[slot];
-          if (kk == y) {
-            uint32_t j = hidx[slot];
-            atomicOr(&sym[size_t(i) * wp + (j >> 5)], 1u << (j & 31));
-            atomicOr(&sym[size_t(j) * wp + (i >> 5)], 1u << (i & 31));
-            break;
-          }
-          if (kk == EMPTY) break;
-          slot = (slot + 1) & tmask;
+    // membership table + the non-empty rows with their prefix positions,
+    // long rows (>= 32 elements) first, then short ones (pass 1); one
+    // packed (rows << 40 | elements) block scan per NT rows
+    uint32_t nl = 0, Ll = 0, ns = 0, Ls = 0;
+    for (int pass = 0; pass < 2; pass++) {
+      uint32_t nr = 0, Lsum = 0;
+      uint32_t* P = pass ? rP + nl + 1 : rP;
+      ull* rb_out = pass ? rbase + nl : rbase;
+      uint32_t* id_out = pass ? rowid + nl : rowid;
+      for (uint32_t t0 = 0; t0 < d; t0 += NT) {
+        const uint32_t i = t0 + threadIdx.x;
+        uint32_t len = 0;
+        uint64_t rb = 0;
+        if (i < d) {
+          const uint32_t w = a.adj[b + i];
+          if (pass == 0) member_insert(M, w, i);
+          rb = a.off[w];
+          len = uint32_t(a.off[w + 1] - rb);
+          if (pass == 0 ? len < 32 : (len == 0 || len >= 32)) len = 0;
         }
+        const ull v = (len ? (1ull << 40) : 0ull) | len;
+        ull excl, agg;
+        BlockScanU64(s_scan).ExclusiveSum(v, excl, agg);
+        if (len) {
+          const uint32_t ci = nr + uint32_t(excl >> 40);
+          P[ci] = Lsum + uint32_t(excl & ((1ull << 40) - 1));
+          rb_out[ci] = rb;
+          id_out[ci] = i;
+        }
+        nr += uint32_t(agg >> 40);
+        Lsum += uint32_t(agg & ((1ull << 40) - 1));
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) P[nr] = Lsum;
+      if (pass == 0) {
+        nl = nr;
+        Ll = Lsum;
+      } else {
+        ns = nr;
+        Ls = Lsum;
       }
     }
+    if (threadIdx.x == 0) my_staged += Ll + Ls;
     __syncthreads();
-    // one warp per oriented edge (u, w_i), dynamically scheduled
+    // stage the induced subgraph: each warp one contiguous 1/NW of the
+    // long-row elements and of the short-row elements
+    {
+      const Rows rl{rP, rbase, rowid, nl};
+      stage_long(rl, M, a.adj, sym, wp, uint32_t(uint64_t(Ll) * wib / NW),
+                 uint32_t(uint64_t(Ll) * (wib + 1) / NW), lane);
+      const Rows rs{rP + nl + 1, rbase + nl, rowid + nl, ns};
+      stage_range(rs, M, a.adj, sym, wp, uint32_t(uint64_t(Ls) * wib / NW),
+                  uint32_t(uint64_t(Ls) * (wib + 1) / NW), lane);
+    }
+    __syncthreads();
+    // one warp per oriented edge (u, w_i) of this item's slice,
+    // dynamically scheduled (low i first: the largest rows)
     ull warp_src = 0;
     for (;;) {
-      uint32_t i = 0;
-      if (lane == 0) i = atomicAdd(&s_edge, 1u);
-      i = __shfl_sync(FULL, i, 0);
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(&s_edge, 1u);
+      const uint32_t i = slice + nsl * __shfl_sync(FULL, t, 0);
       if (i >= d) break;
       // S0 = row i above i
       uint32_t n = 0;
@@ -629,7 +798,7 @@ __global__ void __launch_bounds__(CTA_THREADS) count_cta_kernel(CtaArgs a) {
       }
       __syncwarp();
       const uint32_t s0 = __reduce_add_sync(FULL, n);
-      ull ce = (s0 >= uint32_t(R)) ? warp_count<PV>(c, s0, R) : 0ull;
+      ull ce = (s0 >= uint32_t(R)) ? warp_count<PV, MAXL>(c, s0, R) : 0ull;
       warp_src += ce;
       if constexpr (PV) {
         if (lane == 0 && ce) atomicAdd(&pvl[i], ce);
@@ -641,7 +810,7 @@ __global__ void __launch_bounds__(CTA_THREADS) count_cta_kernel(CtaArgs a) {
     }
     __syncthreads();
     if constexpr (PV) {
-      for (uint32_t i = threadIdx.x; i < d; i += CTA_THREADS)
+      for (uint32_t i = threadIdx.x; i < d; i += NT)
         if (pvl[i]) atomicAdd(&a.pv_rank[a.adj[b + i]], pvl[i]);
       if (threadIdx.x == 0 && s_src_total) atomicAdd(&a.pv_rank[u], s_src_total);
     }
@@ -703,36 +872,55 @@ __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t
     pv[v] = pv_rank[rank[v]];
 }
 
-template <bool PV>
-void launch_cta(Graph& g, CtaArgs a, uint32_t nsrc, bool global_ws, size_t heavy_budget,
-                unsigned* work_ctr) {
-  a.nsrc = nsrc;
-  a.work = work_ctr;
-  KCG_CUDA(cudaMemsetAsync(work_ctr, 0, 4, g.stream));
+template <bool PV, bool GWS, int NT, int MAXL>
+void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget) {
   const Device& dev = device();
+  auto kern = count_cta_kernel<PV, GWS, NT, MAXL>;
   unsigned grid;
   size_t smem = 0;
-  if (!global_ws) {
+  if (!GWS) {
     smem = a.L.total;
-    KCG_CUDA(cudaFuncSetAttribute(count_cta_kernel<PV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem)));
+    KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
-    KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, count_cta_kernel<PV>,
-                                                           CTA_THREADS, smem));
-    occ = std::max(occ, 1);
-    grid = std::min<uint64_t>(nsrc, uint64_t(dev.sms) * occ);
-    a.global_ws = 0;
-    a.gbase = nullptr;
+    KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
+    grid = unsigned(std::min<uint64_t>(a.nitems, uint64_t(dev.sms) * std::max(occ, 1)));
   } else {
-    size_t per = a.L.total;
-    uint64_t fit = std::max<uint64_t>(1, heavy_budget / per);
-    grid = unsigned(std::min<uint64_t>({nsrc, uint64_t(dev.sms) * 2, fit}));
+    const size_t per = a.L.total;
+    const uint64_t fit = std::max<uint64_t>(1, heavy_budget / per);
+    grid = unsigned(std::min<uint64_t>({a.nitems, uint64_t(dev.sms) * 2, fit}));
     a.gbase = g.heavy.ensure(size_t(grid) * per, &g.bytes);
-    a.global_ws = 1;
   }
-  count_cta_kernel<PV><<<grid, CTA_THREADS, smem, g.stream>>>(a);
+  kern<<<grid, NT, smem, g.stream>>>(a);
   KCG_LAUNCHED(g);
   g.stats.launches++;
+}
+
+template <bool PV, int MAXL>
+void launch_cta(Graph& g, CtaArgs a, bool global_ws, int nt, size_t heavy_budget) {
+  KCG_CUDA(cudaMemsetAsync(a.work, 0, 4, g.stream));
+  if (global_ws)
+    launch_cta_t<PV, true, 512, MAXL>(g, a, heavy_budget);
+  else if (nt == 512)
+    launch_cta_t<PV, false, 512, MAXL>(g, a, heavy_budget);
+  else
+    launch_cta_t<PV, false, 256, MAXL>(g, a, heavy_budget);
+}
+
+template <bool PV, int MAXL>
+constexpr size_t stk_bytes() {
+  return sizeof(Stacks<PV, MAXL>);
+}
+inline size_t stacks_size(bool pv, int maxl) {
+  if (pv) return maxl > 8 ? stk_bytes<true, 32>() : stk_bytes<true, 8>();
+  return maxl > 8 ? stk_bytes<false, 32>() : stk_bytes<false, 8>();
+}
+
+// Edge slices per source: for k >= 5 the counting work of a large source
+// (roughly d * s^(k-2)) dwarfs its staging, so its edges are split over
+// several CTAs (each re-stages the bitmap); for k <= 4 staging dominates.
+inline uint32_t slices_for(uint32_t d, int k) {
+  if (k < 5 || d <= 128) return 1;
+  return std::min<uint32_t>(64, d / 64);
 }
 
 inline ull* PVR(Graph& g) { return reinterpret_cast<ull*>(g.pv_rank.p); }
@@ -808,14 +996,24 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     g.sync();
     g.mark(6);
     const Device& dev = device();
-    if (nw) {
+    if (nw && k <= 34) {
+      const bool big = k > 10;
+      const size_t dsm = k >= 5 ? size_t(WARP_TIER_WARPS) * stacks_size(want_pv, big ? 32 : 8) : 0;
+      // kernels without the DFS engine when it cannot run (k <= 4): its
+      // warp-synchronous loop would otherwise shape the code of the whole
+      // kernel
       unsigned grid = blocks_for(uint64_t(nw) * 32, WARP_THREADS_BLOCK, dev.sms * 8u);
+      auto run = [&](auto kern) {
+        KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
+        kern<<<grid, WARP_THREADS_BLOCK, dsm, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, wlist, nw, k,
+                                                          ctr, PVR(g), ctr + 1);
+      };
       if (want_pv)
-        count_warp_kernel<true><<<grid, WARP_THREADS_BLOCK, 0, g.stream>>>(
-            g.rdag_off.p, g.rdag_adj.p, wlist, nw, k, ctr, PVR(g), ctr + 1);
+        k <= 4 ? run(count_warp_kernel<true, 0>)
+               : big ? run(count_warp_kernel<true, 32>) : run(count_warp_kernel<true, 8>);
       else
-        count_warp_kernel<false><<<grid, WARP_THREADS_BLOCK, 0, g.stream>>>(
-            g.rdag_off.p, g.rdag_adj.p, wlist, nw, k, ctr, PVR(g), ctr + 1);
+        k <= 4 ? run(count_warp_kernel<false, 0>)
+               : big ? run(count_warp_kernel<false, 32>) : run(count_warp_kernel<false, 8>);
       KCG_LAUNCHED(g);
       g.stats.launches++;
     }
@@ -823,9 +1021,28 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     if (nc) {
       // bins in descending d: [heavy] (512,1024] (256,512] (128,256] (64,128] (32,64]
       const uint32_t R = uint32_t(k - 2);
-      const uint32_t bounds[] = {SMEM_TIER_MAX, 512, 256, 128, 64, 32};
       auto deg_at = [&](uint32_t i) { return 0xffffffffu - keys[i]; };
-      uint32_t pos = 0;
+      std::vector<uint32_t> verts(nc);
+      KCG_CUDA(cudaMemcpyAsync(verts.data(), clist, size_t(nc) * 4, cudaMemcpyDeviceToHost,
+                               g.stream));
+      g.sync();
+      // work items (source, edge slice), heaviest sources first
+      std::vector<uint32_t> isrc, isl;
+      std::vector<uint32_t> first(nc + 1);
+      for (uint32_t i = 0; i < nc; i++) {
+        first[i] = uint32_t(isrc.size());
+        const uint32_t ns = slices_for(deg_at(i), k);
+        for (uint32_t s = 0; s < ns; s++) {
+          isrc.push_back(verts[i]);
+          isl.push_back((s << 16) | ns);
+        }
+      }
+      first[nc] = uint32_t(isrc.size());
+      const size_t ni = isrc.size();
+      uint32_t* d_items = reinterpret_cast<uint32_t*>(g.scratch3.ensure(ni * 8 + 16, &g.bytes));
+      KCG_CUDA(cudaMemcpyAsync(d_items, isrc.data(), ni * 4, cudaMemcpyHostToDevice, g.stream));
+      KCG_CUDA(cudaMemcpyAsync(d_items + ni, isl.data(), ni * 4, cudaMemcpyHostToDevice,
+                               g.stream));
       unsigned* work = cnt + 2;
       int wslot = 0;
       CtaArgs a{};
@@ -835,35 +1052,50 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       a.total = ctr;
       a.pv_rank = PVR(g);
       a.staged = ctr + 1;
-      // heavy: d > SMEM_TIER_MAX (or anything whose layout does not fit)
-      uint32_t hend = 0;
-      while (hend < nc && deg_at(hend) > SMEM_TIER_MAX) hend++;
-      if (hend) {
-        uint32_t dmax = deg_at(0);
-        a.srcs = clist;
-        a.L = make_layout(dmax, std::max<uint32_t>(R, 1), want_pv);
-        const size_t budget = size_t(8) << 30;
-        if (want_pv)
-          launch_cta<true>(g, a, hend, true, budget, work + wslot++);
-        else
-          launch_cta<false>(g, a, hend, true, budget, work + wslot++);
-        g.stats.sources_heavy = hend;
+      const size_t budget = size_t(8) << 30;
+      const uint32_t levels = std::max<uint32_t>(R, 1);
+      const bool big = k > 10;  // DFS engine stack depth 32 instead of 8
+      // the engine runs inside compacted edge sets only when 3+ vertices
+      // remain below the compacted vertex (k >= 6)
+      const size_t sbytes = k >= 6 ? stacks_size(want_pv, big ? 32 : 8) : 0;
+      auto launch = [&](uint32_t lo_src, uint32_t hi_src, const Layout& L, bool gws, int nt) {
+        a.item_src = d_items + first[lo_src];
+        a.item_sl = d_items + ni + first[lo_src];
+        a.nitems = first[hi_src] - first[lo_src];
+        a.L = L;
+        a.work = work + wslot++;
+        if (want_pv) {
+          if (k <= 5)
+            launch_cta<true, 0>(g, a, gws, nt, budget);
+          else
+            big ? launch_cta<true, 32>(g, a, gws, nt, budget)
+                : launch_cta<true, 8>(g, a, gws, nt, budget);
+        } else {
+          if (k <= 5)
+            launch_cta<false, 0>(g, a, gws, nt, budget);
+          else
+            big ? launch_cta<false, 32>(g, a, gws, nt, budget)
+                : launch_cta<false, 8>(g, a, gws, nt, budget);
+        }
+      };
+      // heavy: d > SMEM_TIER_MAX, working sets in global memory
+      uint32_t pos = 0;
+      while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
+      if (pos) {
+        launch(0, pos, make_layout(deg_at(0), levels, want_pv, 16, sbytes), true, 512);
+        g.stats.sources_heavy = pos;
       }
-      pos = hend;
+      const uint32_t bounds[] = {SMEM_TIER_MAX, 512, 256, 128, 64, 32};
       for (int bi = 0; bi < 5 && pos < nc; bi++) {
         const uint32_t hi = bounds[bi], lo = bounds[bi + 1];
         uint32_t end = pos;
         while (end < nc && deg_at(end) > lo) end++;
         if (end == pos) continue;
-        Layout Lb = make_layout(hi, std::max<uint32_t>(R, 1), want_pv);
-        bool global_ws = Lb.total > size_t(dev.smem_optin) - 1024;
-        a.srcs = clist + pos;
-        a.L = global_ws ? make_layout(deg_at(pos), std::max<uint32_t>(R, 1), want_pv) : Lb;
-        const size_t budget = size_t(8) << 30;
-        if (want_pv)
-          launch_cta<true>(g, a, end - pos, global_ws, budget, work + wslot++);
-        else
-          launch_cta<false>(g, a, end - pos, global_ws, budget, work + wslot++);
+        const int nt = hi > 512 ? 512 : 256;
+        Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes);
+        const bool gws = Lb.total > size_t(dev.smem_optin) - 1024;
+        if (gws) Lb = make_layout(deg_at(pos), levels, want_pv, 16, sbytes);
+        launch(pos, end, Lb, gws, gws ? 512 : nt);
         g.stats.sources_cta += end - pos;
         pos = end;
       }

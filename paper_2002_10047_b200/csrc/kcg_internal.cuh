@@ -129,6 +129,7 @@ struct Graph {
   DevBuf<uint64_t> pv_rank, pv;
   DevBuf<unsigned char> scratch;   // CUB temp + misc
   DevBuf<unsigned char> scratch2;  // per-call work arrays
+  DevBuf<unsigned char> scratch3;  // counting work items
   DevBuf<unsigned char> heavy;     // heavy-tier global bitmaps
   DevBuf<unsigned long long> counters;  // small device counters
   PinnedBuf pinned;
