@@ -288,9 +288,8 @@ def run_kcg(args):
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-        ct = torch.tensor([part_total], dtype=torch.int64, device="cuda")
-        dist.all_reduce(ct)
-        total = int(ct.item()) % (1 << 64)
+        from paper_2002_10047_b200 import shard
+        total, _ = shard.allreduce_counts(part_total, None, device="cuda")
         dist.barrier()
     ms_per_step = ms / args.steps
     value = total / (ms_per_step / 1e3)

@@ -308,3 +308,57 @@ uint64_t kco_alg_bytes(uint32_t n, const uint64_t* out_off, const uint32_t* out_
   free(indeg);
   return 16 * (uint64_t)n + 20 * m + 4 * s;
 }
+
+/* The multi-GPU split of kcg_count_part, restated for the CPU tests: only
+ * the cliques whose lowest-ranked vertex v has rank[v] % nparts == part
+ * (edge tasks (v,u) of counting.cpp:158-187 with such a source v). */
+int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
+                   const uint32_t* rank, int k, uint32_t part, uint32_t nparts,
+                   uint64_t* total_out, uint64_t* pv) {
+  if (k < 2 || nparts == 0 || part >= nparts) return 1;
+  uint64_t total = 0;
+  if (pv) memset(pv, 0, (size_t)n * 8);
+  uint64_t maxd = 0;
+  for (uint32_t v = 0; v < n; v++)
+    if (out_off[v + 1] - out_off[v] > maxd) maxd = out_off[v + 1] - out_off[v];
+  kco_ctx c;
+  c.off = out_off;
+  c.adj = out_adj;
+  c.pv = pv;
+  c.stamp = calloc((size_t)n + 1, 8);
+  c.chain = malloc(((size_t)k + 2) * 4);
+  c.bufs = malloc(((size_t)k + 3) * sizeof(uint32_t*));
+  if (!c.stamp || !c.chain || !c.bufs) return 3;
+  for (int i = 0; i < k + 3; i++) c.bufs[i] = malloc((maxd + 1) * 4);
+  uint64_t next_token = 1;
+  for (uint32_t v = 0; v < n; v++) {
+    if (rank[v] % nparts != part) continue;
+    for (uint64_t e = out_off[v]; e < out_off[v + 1]; e++) {
+      uint32_t u = out_adj[e];
+      if (k == 2) {
+        total++;
+        if (pv) pv[v]++, pv[u]++;
+        continue;
+      }
+      uint32_t* both = c.bufs[2];
+      uint64_t nb = 0, a = out_off[v], b = out_off[u];
+      while (a < out_off[v + 1] && b < out_off[u + 1]) {
+        if (out_adj[a] < out_adj[b]) a++;
+        else if (out_adj[b] < out_adj[a]) b++;
+        else { both[nb++] = out_adj[a]; a++; b++; }
+      }
+      if (nb + 2 < (uint64_t)k) continue;
+      uint64_t tb = next_token;
+      next_token += (uint64_t)k + 2;
+      for (uint64_t i = 0; i < nb; i++) c.stamp[both[i]] = tb + 2;
+      c.chain[0] = v;
+      c.chain[1] = u;
+      c.chain_len = 2;
+      total += kco_rec(&c, both, nb, k - 2, 2, tb);
+    }
+  }
+  *total_out = total;
+  for (int i = 0; i < k + 3; i++) free(c.bufs[i]);
+  free(c.bufs), free(c.chain), free(c.stamp);
+  return 0;
+}

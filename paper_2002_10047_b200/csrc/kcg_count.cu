@@ -776,10 +776,47 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
                   uint32_t(uint64_t(Ls) * (wib + 1) / NW), lane);
     }
     __syncthreads();
+    ull warp_src = 0;
+    if (R == 2) {
+      // k = 4: the source's count is the number of triangles of its induced
+      // DAG, sum over induced edges (i, x) of |N+(i) ∩ N+(x)|.  Every
+      // thread takes upper-triangle bitmap words (i, w) and pops its pairs;
+      // no per-edge scheduling or member gather.
+      ull acc = 0;
+      for (uint32_t q = threadIdx.x; q < d * W; q += NT) {
+        const uint32_t i = q / W, w = q - i * W;
+        if (w < (i >> 5)) continue;
+        const uint32_t* ri = sym + size_t(i) * wp;
+        uint32_t bits = ri[w];
+        if (w == (i >> 5)) bits &= above_mask(i & 31);
+        ull ci = 0;
+        while (bits) {
+          const uint32_t x = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const uint32_t* rx = sym + size_t(x) * wp;
+          uint32_t cx = __popc(ri[w] & rx[w] & above_mask(x & 31));
+          for (uint32_t w2 = w + 1; w2 < W; w2++) cx += __popc(ri[w2] & rx[w2]);
+          ci += cx;
+          if constexpr (PV) {
+            // x's degree inside N+(u) ∩ N+(i): also counts the 4th-vertex role
+            const uint32_t wi = i >> 5;
+            uint32_t all = cx + __popc(ri[w] & rx[w] & ~above_mask(x & 31) &
+                                       (w == wi ? above_mask(i & 31) : FULL));
+            for (uint32_t w2 = wi; w2 < w; w2++)
+              all += __popc(ri[w2] & rx[w2] & (w2 == wi ? above_mask(i & 31) : FULL));
+            if (all) atomicAdd(&pvl[x], ull(all));
+          }
+        }
+        acc += ci;
+        if constexpr (PV) {
+          if (ci) atomicAdd(&pvl[i], ci);
+        }
+      }
+      warp_src = warp_sum(acc);
+    }
     // one warp per oriented edge (u, w_i) of this item's slice,
     // dynamically scheduled (low i first: the largest rows)
-    ull warp_src = 0;
-    for (;;) {
+    for (; R != 2;) {
       uint32_t t = 0;
       if (lane == 0) t = atomicAdd(&s_edge, 1u);
       const uint32_t i = slice + nsl * __shfl_sync(FULL, t, 0);
