@@ -57,176 +57,13 @@ __device__ __forceinline__ ull warp_sum(ull v) {
   return v;
 }
 
-// ---------------------------------------------------------------------------
-// Staging: membership test for N+(u) and the flattened scan of its rows.
-// ---------------------------------------------------------------------------
-constexpr ull EMPTY64 = ~0ull;
+}  // namespace
+}  // namespace kcg
 
-// Open-addressing table of (key | local index << 32) plus a 1-bit-per-slot
-// filter; most probes of a scan miss and cost one shared load of the
-// filter word.
-struct Member {
-  ull* table;
-  uint32_t* filter;
-  uint32_t tbits, fbits;
-};
+#include "kcg_stage.cuh"
 
-__device__ __forceinline__ void member_insert(const Member& M, uint32_t key, uint32_t idx) {
-  const uint32_t h = key * 0x9E3779B1u;
-  const uint32_t fb = h >> (32 - M.fbits);
-  atomicOr(&M.filter[fb >> 5], 1u << (fb & 31));
-  const uint32_t mask = (1u << M.tbits) - 1;
-  uint32_t slot = h >> (32 - M.tbits);
-  const ull packed = ull(key) | (ull(idx) << 32);
-  while (atomicCAS(&M.table[slot], EMPTY64, packed) != EMPTY64) slot = (slot + 1) & mask;
-}
-
-__device__ __forceinline__ uint32_t member_find(const Member& M, uint32_t key) {
-  const uint32_t h = key * 0x9E3779B1u;
-  const uint32_t fb = h >> (32 - M.fbits);
-  if (!((M.filter[fb >> 5] >> (fb & 31)) & 1u)) return NOTFOUND;
-  const uint32_t mask = (1u << M.tbits) - 1;
-  uint32_t slot = h >> (32 - M.tbits);
-  for (;;) {
-    const ull e = M.table[slot];
-    if (uint32_t(e) == key) return uint32_t(e >> 32);
-    if (uint32_t(e) == EMPTY) return NOTFOUND;
-    slot = (slot + 1) & mask;
-  }
-}
-
-// Non-empty rows of a source in local order: row r is N+(w_rowid[r]),
-// global elements adj[rbase[r] ..), first virtual position P[r]; P[nr] = L.
-struct Rows {
-  const uint32_t* P;
-  const ull* rbase;
-  const uint32_t* rowid;
-  uint32_t nr;
-};
-
-// One warp stages virtual positions [pbeg, pend) of the concatenated rows:
-// 32 consecutive elements per chunk, one per lane; a lane finds its row
-// from the bitmask of row starts inside the chunk (one REDUX.OR); STAGE_U
-// chunks issue their global loads before any lookup so several loads per
-// lane are in flight.  Every hit j in row i sets sym(i, j) and sym(j, i).
-constexpr int STAGE_U = 4;
-
-__device__ __forceinline__ void stage_range(const Rows& R, const Member& M,
-                                            const uint32_t* __restrict__ adj, uint32_t* sym,
-                                            uint32_t wp, uint32_t pbeg, uint32_t pend,
-                                            uint32_t lane) {
-  if (pbeg >= pend) return;
-  uint32_t lo = 0, hi = R.nr;  // P[lo] <= pbeg < P[hi]
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (R.P[mid] <= pbeg)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  uint32_t cur = lo, pcur = R.P[lo];
-  const uint32_t le_mask = (2u << lane) - 1u;
-  for (uint32_t c0 = pbeg; c0 < pend; c0 += 32 * STAGE_U) {
-    // reconverge after the previous chunk's data-dependent probe loops so
-    // the REDUX/VOTE/SHFL below take the converged fast path
-    __syncwarp();
-    uint32_t y[STAGE_U], row[STAGE_U];
-#pragma unroll
-    for (int u = 0; u < STAGE_U; u++) {
-      const uint32_t cb = c0 + 32 * u;
-      const uint32_t p = cb + lane;
-      const uint32_t jn = cur + 1 + lane;
-      const uint32_t pn = jn <= R.nr ? R.P[jn] : 0xffffffffu;
-      const uint32_t rel = pn - cb;
-      const uint32_t starts = __reduce_or_sync(FULL, rel < 32u ? (1u << rel) : 0u);
-      const uint32_t kk = __popc(starts & le_mask);
-      const uint32_t seg = cur + kk;
-      uint32_t pseg = __shfl_sync(FULL, pn, (kk - 1) & 31);
-      if (kk == 0) pseg = pcur;
-      const uint32_t adv = __popc(__ballot_sync(FULL, pn <= cb + 32));
-      const uint32_t pnext = __shfl_sync(FULL, pn, (adv - 1) & 31);
-      if (adv) pcur = pnext;
-      cur += adv;
-      y[u] = EMPTY;
-      row[u] = 0;
-      if (p < pend) {
-        y[u] = __ldg(adj + R.rbase[seg] + (p - pseg));
-        row[u] = R.rowid[seg];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < STAGE_U; u++) {
-      if (y[u] != EMPTY) {
-        const uint32_t j = member_find(M, y[u]);
-        if (j != NOTFOUND) {
-          const uint32_t i = row[u];
-          atomicOr(&sym[size_t(i) * wp + (j >> 5)], 1u << (j & 31));
-          atomicOr(&sym[size_t(j) * wp + (i >> 5)], 1u << (i & 31));
-        }
-      }
-    }
-  }
-}
-
-// Rows of >= 32 elements: a 32-element chunk touches at most two rows, so a
-// lane's row is one compare against the warp-uniform boundary pnext.
-__device__ __forceinline__ void stage_long(const Rows& R, const Member& M,
-                                           const uint32_t* __restrict__ adj, uint32_t* sym,
-                                           uint32_t wp, uint32_t pbeg, uint32_t pend,
-                                           uint32_t lane) {
-  if (pbeg >= pend) return;
-  uint32_t lo = 0, hi = R.nr;  // P[lo] <= pbeg < P[hi]
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (R.P[mid] <= pbeg)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  uint32_t cur = lo;
-  uint32_t pnext = R.P[cur + 1];
-  ull bcur = R.rbase[cur] - R.P[cur];
-  uint32_t rcur = R.rowid[cur];
-  ull bnxt = 0;
-  uint32_t rnxt = 0;
-  if (cur + 1 < R.nr) {
-    bnxt = R.rbase[cur + 1] - pnext;
-    rnxt = R.rowid[cur + 1];
-  }
-  for (uint32_t c0 = pbeg; c0 < pend; c0 += 32 * STAGE_U) {
-    uint32_t y[STAGE_U], row[STAGE_U];
-#pragma unroll
-    for (int u = 0; u < STAGE_U; u++) {
-      const uint32_t cb = c0 + 32 * u;
-      const uint32_t p = cb + lane;
-      const bool nx = p >= pnext;
-      y[u] = EMPTY;
-      row[u] = nx ? rnxt : rcur;
-      if (p < pend) y[u] = __ldg(adj + (nx ? bnxt : bcur) + p);
-      if (cb + 32 >= pnext && cb + 32 < pend) {  // warp-uniform row advance
-        cur++;
-        bcur = bnxt;
-        rcur = rnxt;
-        pnext = R.P[cur + 1];
-        if (cur + 1 < R.nr) {
-          bnxt = R.rbase[cur + 1] - pnext;
-          rnxt = R.rowid[cur + 1];
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < STAGE_U; u++) {
-      if (y[u] != EMPTY) {
-        const uint32_t j = member_find(M, y[u]);
-        if (j != NOTFOUND) {
-          const uint32_t i = row[u];
-          atomicOr(&sym[size_t(i) * wp + (j >> 5)], 1u << (j & 31));
-          atomicOr(&sym[size_t(j) * wp + (i >> 5)], 1u << (i & 31));
-        }
-      }
-    }
-  }
-}
+namespace kcg {
+namespace {
 
 }  // namespace
 }  // namespace kcg
@@ -254,6 +91,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     uint32_t rowid[32];
     uint32_t filter[16];
     uint32_t map[32];
+    uint32_t qy[64], qi[64];
   };
   __shared__ WarpSmem s_w[WARP_TIER_WARPS];
   __shared__ ull s_pv[PV ? WARP_TIER_WARPS : 1][32];
@@ -287,10 +125,16 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     }
     __syncwarp();
     if (lane < d) member_insert(M, w, lane);
-    // split the non-empty rows into long (>= 32) and short ones, each list
-    // compacted with its own prefix of lengths; long rows at [0, nl),
-    // short rows at [nl, nl + ns) with their prefix at P[nl + 1 ..]
-    const bool lg = len >= 32, sh = len > 0 && len < 32;
+    // Row i either is scanned (len entries) or searched: its d-1-i
+    // candidate targets w_j (j > i) are binary-searched in N+(w_i), which
+    // costs (d-1-i) * log2(len) probes -- cheaper for the long rows that
+    // small sources point into.
+    const uint32_t tg = lane < d ? d - 1 - lane : 0u;
+    const bool srch = tg > 0 && tg * (32u - __clz(len)) < len;
+    // split the other non-empty rows into long (>= 32) and short ones,
+    // each list compacted with its own prefix of lengths; long rows at
+    // [0, nl), short rows at [nl, nl + ns) with their prefix at P[nl + 1 ..]
+    const bool lg = !srch && len >= 32, sh = !srch && len > 0 && len < 32;
     const unsigned ml = __ballot_sync(FULL, lg), ms = __ballot_sync(FULL, sh);
     const uint32_t nl = __popc(ml), ns = __popc(ms);
     uint32_t il = lg ? len : 0, is = sh ? len : 0;
@@ -318,13 +162,52 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
       S.P[nl] = Ll;
       S.P[nl + 1 + ns] = Ls;
     }
-    my_staged += len;
+    my_staged += srch ? 0u : len;
     __syncwarp();
     {
+      // searched rows: tasks (i, j) flattened over the lanes
+      uint32_t ti = srch ? tg : 0u;
+      for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, ti, s);
+        if (lane >= uint32_t(s)) ti += t;
+      }
+      const uint32_t T = __shfl_sync(FULL, ti, 31);
+      const uint32_t tex = ti - (srch ? tg : 0u);
+      for (uint32_t t0 = 0; t0 < T; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        uint32_t r = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const uint32_t cand = r + step;
+          const uint32_t pe = __shfl_sync(FULL, tex, cand);
+          if (pe <= t && cand < d) r = cand;
+        }
+        const uint32_t rt = __shfl_sync(FULL, tex, r);
+        const uint64_t rb = __shfl_sync(FULL, sb, r);
+        const uint32_t rl = __shfl_sync(FULL, len, r);
+        const uint32_t j = r + 1 + (t - rt);
+        const uint32_t target = __shfl_sync(FULL, w, j & 31);
+        if (t < T) {
+          // lower_bound(target) in the sorted row adj[rb, rb + rl)
+          uint32_t lo = 0, n = rl;
+          while (n > 1) {
+            const uint32_t half = n >> 1;
+            if (__ldg(adj + rb + lo + half - 1) < target) lo += half;
+            n -= half;
+          }
+          if (__ldg(adj + rb + lo) == target) {
+            atomicOr(&sym[r], 1u << j);
+            atomicOr(&sym[j], 1u << r);
+          }
+        }
+      }
+      my_staged += T;
+      Stager st{M, sym, 1, S.qy, S.qi, lane, 0};
       const Rows rl{S.P, S.rbase, S.rowid, nl};
-      stage_long(rl, M, adj, sym, 1, 0, Ll, lane);
+      stage_long(rl, st, adj, 0, Ll);
       const Rows rs{S.P + nl + 1, S.rbase + nl, S.rowid + nl, ns};
-      stage_range(rs, M, adj, sym, 1, 0, Ls, lane);
+      stage_short(rs, st, adj, 0, Ls);
+      st.flush();
     }
     __syncwarp();
     S.usym[lane] = sym[lane] & above_mask(lane);
@@ -374,7 +257,7 @@ struct Layout {
   uint32_t dmax, wpmax, tbits, fbits, levels;
   size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
   // per-warp offsets
-  size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk;
+  size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk, w_q;
   size_t total;
 };
 
@@ -421,6 +304,8 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   w = align_up(w + size_t(levels) * sizeof(Lvl), 16);
   L.w_stk = w;
   w = align_up(w + stk_bytes, 16);
+  L.w_q = w;
+  w = align_up(w + 128 * 4, 16);
   L.warp_stride = w;
   L.total = align_up(at + w * nw, 128);
   return L;
@@ -434,6 +319,7 @@ struct WarpCtx {
   uint32_t* csym;       // 32 words: compact rows, both directions
   uint32_t* cusym;      // 32 words: compact rows, upper part
   void* stk;            // Stacks<PV, MAXL> of the warp's DFS engine
+  uint32_t* qy;         // 128 words: staging queue (keys, rows)
   ull* cpv;             // 32 (PV)
   ull* pvl;             // d (PV)
   Lvl* lvl;
@@ -688,6 +574,7 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
   c.csym = reinterpret_cast<uint32_t*>(wbase + L.w_csym);
   c.cusym = reinterpret_cast<uint32_t*>(wbase + L.w_cusym);
   c.stk = wbase + L.w_stk;
+  c.qy = reinterpret_cast<uint32_t*>(wbase + L.w_q);
   c.cpv = reinterpret_cast<ull*>(wbase + L.w_cpv);
   c.lvl = reinterpret_cast<Lvl*>(wbase + L.w_lvl);
   c.pvl = pvl;
@@ -768,12 +655,14 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
     // stage the induced subgraph: each warp one contiguous 1/NW of the
     // long-row elements and of the short-row elements
     {
+      Stager st{M, sym, wp, c.qy, c.qy + 64, lane, 0};
       const Rows rl{rP, rbase, rowid, nl};
-      stage_long(rl, M, a.adj, sym, wp, uint32_t(uint64_t(Ll) * wib / NW),
-                 uint32_t(uint64_t(Ll) * (wib + 1) / NW), lane);
+      stage_long(rl, st, a.adj, uint32_t(uint64_t(Ll) * wib / NW),
+                 uint32_t(uint64_t(Ll) * (wib + 1) / NW));
       const Rows rs{rP + nl + 1, rbase + nl, rowid + nl, ns};
-      stage_range(rs, M, a.adj, sym, wp, uint32_t(uint64_t(Ls) * wib / NW),
-                  uint32_t(uint64_t(Ls) * (wib + 1) / NW), lane);
+      stage_short(rs, st, a.adj, uint32_t(uint64_t(Ls) * wib / NW),
+                  uint32_t(uint64_t(Ls) * (wib + 1) / NW));
+      st.flush();
     }
     __syncthreads();
     ull warp_src = 0;
