@@ -83,12 +83,22 @@ Graph::Graph() {
   device();
   KCG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   for (auto& e : ev) KCG_CUDA(cudaEventCreate(&e));
+  for (auto& s : aux) KCG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  KCG_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+  for (auto& e : join_ev) KCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 Graph::~Graph() {
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& s : aux)
+    if (s) cudaStreamSynchronize(s);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : join_ev)
+    if (e) cudaEventDestroy(e);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  for (auto& s : aux)
+    if (s) cudaStreamDestroy(s);
   if (stream) cudaStreamDestroy(stream);
 }
 

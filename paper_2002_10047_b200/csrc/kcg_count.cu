@@ -799,7 +799,7 @@ __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t
 }
 
 template <bool PV, bool GWS, int NT, int MAXL>
-void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget) {
+void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget, cudaStream_t st) {
   const Device& dev = device();
   auto kern = count_cta_kernel<PV, GWS, NT, MAXL>;
   unsigned grid;
@@ -814,22 +814,24 @@ void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget) {
     const size_t per = a.L.total;
     const uint64_t fit = std::max<uint64_t>(1, heavy_budget / per);
     grid = unsigned(std::min<uint64_t>({a.nitems, uint64_t(dev.sms) * 2, fit}));
-    a.gbase = g.heavy.ensure(size_t(grid) * per, &g.bytes);
+    a.gbase = g.heavy.p;  // sized by the caller before any launch
+    if (size_t(grid) * per > g.heavy.n) fail(KCG_ERUNTIME, "heavy arena too small");
   }
-  kern<<<grid, NT, smem, g.stream>>>(a);
+  kern<<<grid, NT, smem, st>>>(a);
   KCG_LAUNCHED(g);
   g.stats.launches++;
 }
 
 template <bool PV, int MAXL>
-void launch_cta(Graph& g, CtaArgs a, bool global_ws, int nt, size_t heavy_budget) {
-  KCG_CUDA(cudaMemsetAsync(a.work, 0, 4, g.stream));
+void launch_cta(Graph& g, CtaArgs a, bool global_ws, int nt, size_t heavy_budget,
+                cudaStream_t st) {
+  KCG_CUDA(cudaMemsetAsync(a.work, 0, 4, st));
   if (global_ws)
-    launch_cta_t<PV, true, 512, MAXL>(g, a, heavy_budget);
+    launch_cta_t<PV, true, 512, MAXL>(g, a, heavy_budget, st);
   else if (nt == 512)
-    launch_cta_t<PV, false, 512, MAXL>(g, a, heavy_budget);
+    launch_cta_t<PV, false, 512, MAXL>(g, a, heavy_budget, st);
   else
-    launch_cta_t<PV, false, 256, MAXL>(g, a, heavy_budget);
+    launch_cta_t<PV, false, 256, MAXL>(g, a, heavy_budget, st);
 }
 
 template <bool PV, int MAXL>
@@ -922,6 +924,17 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     g.sync();
     g.mark(6);
     const Device& dev = device();
+    // the tier launches are independent (they only add into the totals):
+    // fork them over the handle's auxiliary streams and join before mark(7)
+    KCG_CUDA(cudaEventRecord(g.fork_ev, g.stream));
+    for (int i = 0; i < Graph::kAux; i++) KCG_CUDA(cudaStreamWaitEvent(g.aux[i], g.fork_ev, 0));
+    int next_aux = 1;  // aux[0] serialises the global-memory (heavy) launches
+    auto aux_stream = [&](bool gws) {
+      if (gws) return g.aux[0];
+      cudaStream_t s = g.aux[next_aux];
+      next_aux = next_aux % (Graph::kAux - 1) + 1;
+      return s;
+    };
     if (nw && k <= 34) {
       const bool big = k > 10;
       const size_t dsm = k >= 5 ? size_t(WARP_TIER_WARPS) * stacks_size(want_pv, big ? 32 : 8) : 0;
@@ -931,7 +944,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       unsigned grid = blocks_for(uint64_t(nw) * 32, WARP_THREADS_BLOCK, dev.sms * 8u);
       auto run = [&](auto kern) {
         KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
-        kern<<<grid, WARP_THREADS_BLOCK, dsm, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, wlist, nw, k,
+        kern<<<grid, WARP_THREADS_BLOCK, dsm, aux_stream(false)>>>(g.rdag_off.p, g.rdag_adj.p, wlist, nw, k,
                                                           ctr, PVR(g), ctr + 1);
       };
       if (want_pv)
@@ -984,35 +997,25 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       // the engine runs inside compacted edge sets only when 3+ vertices
       // remain below the compacted vertex (k >= 6)
       const size_t sbytes = k >= 6 ? stacks_size(want_pv, big ? 32 : 8) : 0;
-      auto launch = [&](uint32_t lo_src, uint32_t hi_src, const Layout& L, bool gws, int nt) {
-        a.item_src = d_items + first[lo_src];
-        a.item_sl = d_items + ni + first[lo_src];
-        a.nitems = first[hi_src] - first[lo_src];
-        a.L = L;
-        a.work = work + wslot++;
-        if (want_pv) {
-          if (k <= 5)
-            launch_cta<true, 0>(g, a, gws, nt, budget);
-          else
-            big ? launch_cta<true, 32>(g, a, gws, nt, budget)
-                : launch_cta<true, 8>(g, a, gws, nt, budget);
-        } else {
-          if (k <= 5)
-            launch_cta<false, 0>(g, a, gws, nt, budget);
-          else
-            big ? launch_cta<false, 32>(g, a, gws, nt, budget)
-                : launch_cta<false, 8>(g, a, gws, nt, budget);
-        }
+      struct Plan {
+        uint32_t lo, hi;
+        Layout L;
+        bool gws;
+        int nt;
       };
+      std::vector<Plan> plans;
       // heavy: d > SMEM_TIER_MAX, working sets in global memory
       uint32_t pos = 0;
       while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
       if (pos) {
-        launch(0, pos, make_layout(deg_at(0), levels, want_pv, 16, sbytes), true, 512);
+        plans.push_back({0, pos, make_layout(deg_at(0), levels, want_pv, 16, sbytes), true, 512});
         g.stats.sources_heavy = pos;
       }
-      const uint32_t bounds[] = {SMEM_TIER_MAX, 512, 256, 128, 64, 32};
-      for (int bi = 0; bi < 5 && pos < nc; bi++) {
+      // shared-memory bins, sqrt(2) apart so each bin's footprint (and
+      // occupancy) tracks its degrees
+      const uint32_t bounds[] = {SMEM_TIER_MAX, 724, 512, 362, 256, 181, 128, 90, 64, 45, 32};
+      const int nbounds = sizeof(bounds) / sizeof(bounds[0]);
+      for (int bi = 0; bi + 1 < nbounds && pos < nc; bi++) {
         const uint32_t hi = bounds[bi], lo = bounds[bi + 1];
         uint32_t end = pos;
         while (end < nc && deg_at(end) > lo) end++;
@@ -1021,10 +1024,47 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
         Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes);
         const bool gws = Lb.total > size_t(dev.smem_optin) - 1024;
         if (gws) Lb = make_layout(deg_at(pos), levels, want_pv, 16, sbytes);
-        launch(pos, end, Lb, gws, gws ? 512 : nt);
+        plans.push_back({pos, end, Lb, gws, gws ? 512 : nt});
         g.stats.sources_cta += end - pos;
         pos = end;
       }
+      // one heavy arena for all global-memory launches (they run in order
+      // on aux[0])
+      size_t arena = 0;
+      for (const Plan& pl : plans)
+        if (pl.gws) {
+          const uint64_t fit = std::max<uint64_t>(1, budget / pl.L.total);
+          const uint64_t grid = std::min<uint64_t>(
+              {uint64_t(first[pl.hi] - first[pl.lo]), uint64_t(dev.sms) * 2, fit});
+          arena = std::max<size_t>(arena, grid * pl.L.total);
+        }
+      if (arena) g.heavy.ensure(arena, &g.bytes);
+      for (const Plan& pl : plans) {
+        a.item_src = d_items + first[pl.lo];
+        a.item_sl = d_items + ni + first[pl.lo];
+        a.nitems = first[pl.hi] - first[pl.lo];
+        a.L = pl.L;
+        a.work = work + wslot++;
+        cudaStream_t st = aux_stream(pl.gws);
+        if (want_pv) {
+          if (k <= 5)
+            launch_cta<true, 0>(g, a, pl.gws, pl.nt, budget, st);
+          else
+            big ? launch_cta<true, 32>(g, a, pl.gws, pl.nt, budget, st)
+                : launch_cta<true, 8>(g, a, pl.gws, pl.nt, budget, st);
+        } else {
+          if (k <= 5)
+            launch_cta<false, 0>(g, a, pl.gws, pl.nt, budget, st);
+          else
+            big ? launch_cta<false, 32>(g, a, pl.gws, pl.nt, budget, st)
+                : launch_cta<false, 8>(g, a, pl.gws, pl.nt, budget, st);
+        }
+      }
+    }
+    // join the auxiliary streams
+    for (int i = 0; i < Graph::kAux; i++) {
+      KCG_CUDA(cudaEventRecord(g.join_ev[i], g.aux[i]));
+      KCG_CUDA(cudaStreamWaitEvent(g.stream, g.join_ev[i], 0));
     }
     g.mark(7);
   } else {

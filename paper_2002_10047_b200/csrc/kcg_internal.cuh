@@ -137,6 +137,12 @@ struct Graph {
   kcg_times times{};
   kcg_count_stats stats{};
   cudaEvent_t ev[8] = {};
+  // auxiliary streams for concurrent counting launches (fork/join with
+  // events against `stream`)
+  static constexpr int kAux = 6;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t fork_ev = nullptr;
+  cudaEvent_t join_ev[kAux] = {};
 
   Graph();
   ~Graph();
