@@ -68,6 +68,13 @@ const Device& device() {
     g_dev.l2 = p.l2CacheSize;
     g_dev.major = p.major;
     g_dev.minor = p.minor;
+    // keep freed pool memory cached: handles come and go on every call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    (void)cudaGetLastError();
     if (p.major != 10) {
       g_dev_err = "libkcg is built for sm_100a (B200); found compute capability " +
                   std::to_string(p.major) + "." + std::to_string(p.minor);
@@ -82,13 +89,37 @@ const Device& device() {
 Graph::Graph() {
   device();
   KCG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  alloc.stream = stream;
   for (auto& e : ev) KCG_CUDA(cudaEventCreate(&e));
   for (auto& s : aux) KCG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   KCG_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
   for (auto& e : join_ev) KCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
+void Graph::release_all() {
+  und_off.release();
+  und_adj.release();
+  deg.release();
+  rank.release();
+  order.release();
+  dag_off.release();
+  dag_adj.release();
+  rdag_off.release();
+  rdag_adj.release();
+  pv_rank.release();
+  pv.release();
+  scratch.release();
+  scratch2.release();
+  scratch3.release();
+  heavy.release();
+  counters.release();
+}
+
 Graph::~Graph() {
+  for (auto& s : aux)
+    if (s) cudaStreamSynchronize(s);
+  if (stream) cudaStreamSynchronize(stream);
+  release_all();
   if (stream) cudaStreamSynchronize(stream);
   for (auto& s : aux)
     if (s) cudaStreamSynchronize(s);
@@ -111,7 +142,7 @@ double Graph::elapsed(int a, int b) {
   return ms;
 }
 
-void* cub_temp(Graph& g, size_t bytes) { return g.scratch.ensure(bytes, &g.bytes); }
+void* cub_temp(Graph& g, size_t bytes) { return g.scratch.ensure(bytes, &g.alloc); }
 
 namespace {
 
@@ -164,7 +195,7 @@ void download(Graph& g, void* dst, const void* src, size_t bytes) {
 }
 
 void finish_und(Graph& g) {
-  g.deg.ensure(g.n, &g.bytes);
+  g.deg.ensure(g.n, &g.alloc);
   if (g.n)
     degree_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.und_off.p, g.n, g.deg.p);
   KCG_LAUNCHED(g);
@@ -173,11 +204,11 @@ void finish_und(Graph& g) {
 
 void install_rank_device(Graph& g) {
   // rank[] already on device: validate and build order[]
-  uint32_t* seen = reinterpret_cast<uint32_t*>(g.scratch2.ensure(size_t(g.n) * 4 + 8, &g.bytes));
-  g.counters.ensure(4, &g.bytes);
+  uint32_t* seen = reinterpret_cast<uint32_t*>(g.scratch2.ensure(size_t(g.n) * 4 + 8, &g.alloc));
+  g.counters.ensure(4, &g.alloc);
   KCG_CUDA(cudaMemsetAsync(seen, 0, size_t(g.n) * 4, g.stream));
   KCG_CUDA(cudaMemsetAsync(g.counters.p, 0, 8, g.stream));
-  g.order.ensure(g.n, &g.bytes);
+  g.order.ensure(g.n, &g.alloc);
   if (g.n)
     bijection_kernel<<<blocks_for(g.n, 256), 256, 0, g.stream>>>(g.rank.p, g.n, seen,
                                                                    g.order.p, g.counters.p);
@@ -228,8 +259,8 @@ int kcg_graph_create(uint32_t n, const uint64_t* offsets, const uint32_t* adj,
       g->m = two_m / 2;
       g->times = kcg_times{};
       g->mark(0);
-      g->und_off.ensure(size_t(n) + 1, &g->bytes);
-      g->und_adj.ensure(two_m, &g->bytes);
+      g->und_off.ensure(size_t(n) + 1, &g->alloc);
+      g->und_adj.ensure(two_m, &g->alloc);
       upload(*g, g->und_off.p, offsets, (size_t(n) + 1) * 8);
       upload(*g, g->und_adj.p, adj, two_m * 4);
       finish_und(*g);
@@ -252,8 +283,8 @@ int kcg_graph_create_device(uint32_t n, uint64_t m, const uint64_t* d_offsets,
     try {
       g->n = n;
       g->m = m;
-      g->und_off.ensure(size_t(n) + 1, &g->bytes);
-      g->und_adj.ensure(2 * m, &g->bytes);
+      g->und_off.ensure(size_t(n) + 1, &g->alloc);
+      g->und_adj.ensure(2 * m, &g->alloc);
       KCG_CUDA(cudaMemcpyAsync(g->und_off.p, d_offsets, (size_t(n) + 1) * 8,
                                cudaMemcpyDeviceToDevice, g->stream));
       if (m)
@@ -284,9 +315,9 @@ int kcg_dag_create(uint32_t n, const uint64_t* out_offsets, const uint32_t* out_
       g->m = m;
       g->times = kcg_times{};
       g->mark(0);
-      g->dag_off.ensure(size_t(n) + 1, &g->bytes);
-      g->dag_adj.ensure(m, &g->bytes);
-      g->rank.ensure(n, &g->bytes);
+      g->dag_off.ensure(size_t(n) + 1, &g->alloc);
+      g->dag_adj.ensure(m, &g->alloc);
+      g->rank.ensure(n, &g->alloc);
       upload(*g, g->dag_off.p, out_offsets, (size_t(n) + 1) * 8);
       upload(*g, g->dag_adj.p, out_targets, m * 4);
       upload(*g, g->rank.p, rank, size_t(n) * 4);
@@ -351,7 +382,7 @@ int kcg_set_ranking(kcg_graph* h, const uint32_t* rank, uint32_t len) {
     Graph& g = *G(h);
     if (len != g.n) fail(KCG_EINVAL, "ranking size does not match graph");
     if (g.n && !rank) fail(KCG_EINVAL, "rank is null");
-    g.rank.ensure(g.n, &g.bytes);
+    g.rank.ensure(g.n, &g.alloc);
     upload(g, g.rank.p, rank, size_t(g.n) * 4);
     install_rank_device(g);
   });
@@ -469,7 +500,7 @@ int kcg_last_count_stats(const kcg_graph* h, kcg_count_stats* out) {
 }
 
 uint64_t kcg_device_bytes(const kcg_graph* h) {
-  return h ? reinterpret_cast<const Graph*>(h)->bytes : 0;
+  return h ? reinterpret_cast<const Graph*>(h)->alloc.bytes : 0;
 }
 
 int kcg_synchronize(kcg_graph* h) {

@@ -863,11 +863,11 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
   g.stats = kcg_count_stats{};
   g.stats.max_out_degree = g.max_out;
   g.mark(2);
-  ull* ctr = g.counters.ensure(16, &g.bytes);  // [0]=total [1]=staged [2..] work counters
+  ull* ctr = g.counters.ensure(16, &g.alloc);  // [0]=total [1]=staged [2..] work counters
   KCG_CUDA(cudaMemsetAsync(ctr, 0, 16 * 8, g.stream));
   if (want_pv) {
-    g.pv_rank.ensure(size_t(n) + 1, &g.bytes);
-    g.pv.ensure(size_t(n) + 1, &g.bytes);
+    g.pv_rank.ensure(size_t(n) + 1, &g.alloc);
+    g.pv.ensure(size_t(n) + 1, &g.alloc);
     KCG_CUDA(cudaMemsetAsync(g.pv_rank.p, 0, size_t(n) * 8, g.stream));
   }
   uint64_t total = 0;
@@ -892,7 +892,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     // tier lists
     const uint32_t dmin = uint32_t(k - 1);
     size_t nb = (size_t(n) * 4 + 255) & ~size_t(255);
-    unsigned char* sb = g.scratch2.ensure(nb * 5 + 1024, &g.bytes);
+    unsigned char* sb = g.scratch2.ensure(nb * 5 + 1024, &g.alloc);
     uint32_t* wlist = reinterpret_cast<uint32_t*>(sb);
     uint32_t* clist = reinterpret_cast<uint32_t*>(sb + nb);
     uint32_t* ckey = reinterpret_cast<uint32_t*>(sb + 2 * nb);
@@ -978,7 +978,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       }
       first[nc] = uint32_t(isrc.size());
       const size_t ni = isrc.size();
-      uint32_t* d_items = reinterpret_cast<uint32_t*>(g.scratch3.ensure(ni * 8 + 16, &g.bytes));
+      uint32_t* d_items = reinterpret_cast<uint32_t*>(g.scratch3.ensure(ni * 8 + 16, &g.alloc));
       KCG_CUDA(cudaMemcpyAsync(d_items, isrc.data(), ni * 4, cudaMemcpyHostToDevice, g.stream));
       KCG_CUDA(cudaMemcpyAsync(d_items + ni, isl.data(), ni * 4, cudaMemcpyHostToDevice,
                                g.stream));
@@ -1038,7 +1038,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
               {uint64_t(first[pl.hi] - first[pl.lo]), uint64_t(dev.sms) * 2, fit});
           arena = std::max<size_t>(arena, grid * pl.L.total);
         }
-      if (arena) g.heavy.ensure(arena, &g.bytes);
+      if (arena) g.heavy.ensure(arena, &g.alloc);
       for (const Plan& pl : plans) {
         a.item_src = d_items + first[pl.lo];
         a.item_sl = d_items + ni + first[pl.lo];

@@ -12,6 +12,7 @@
 //  sort    segmented sort of the relabelled slices (ascending rank), so
 //          every out-neighbourhood is in topological order
 #include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 
@@ -43,20 +44,44 @@ __global__ void outdeg_kernel(const uint64_t* __restrict__ off, const uint32_t* 
   }
 }
 
-__global__ void fill_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                            const uint32_t* __restrict__ rank, uint32_t n,
-                            const uint64_t* __restrict__ dag_off, uint32_t* __restrict__ dag_adj,
-                            const uint64_t* __restrict__ rdag_off,
-                            uint32_t* __restrict__ rdag_adj) {
-  const uint32_t lane = threadIdx.x & 31;
+constexpr uint32_t kMidSortL = 256;
+
+__device__ __forceinline__ uint32_t warp_bitonic_sort(uint32_t x, uint32_t lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+      x = keep_min ? min(x, y) : max(x, y);
+    }
+  }
+  return x;
+}
+
+// Pass 2: ordered compaction of each slice into the id-space DAG (ascending
+// ids, like graph.cpp:102-112) and the relabelled slice of rank[u].
+// Relabelled slices of <= 32 targets are sorted in registers (warp bitonic
+// sort); longer ones are listed for sort_long_kernel.
+__global__ void __launch_bounds__(256)
+    fill_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                const uint32_t* __restrict__ rank, uint32_t n,
+                const uint64_t* __restrict__ dag_off, uint32_t* __restrict__ dag_adj,
+                const uint64_t* __restrict__ rdag_off, uint32_t* __restrict__ rdag_adj,
+                uint32_t* __restrict__ long_list, unsigned* __restrict__ nlong) {
+  __shared__ uint32_t buf[8][32];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n;
        u += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     const uint32_t ru = rank[u];
     const uint64_t b = off[u], e = off[u + 1];
     uint64_t wid = dag_adj ? dag_off[u] : 0;
-    uint64_t wr = rdag_off[ru];
-    for (uint64_t p0 = b; p0 < e; p0 += 32) {
-      uint64_t p = p0 + lane;
+    const uint64_t wr0 = rdag_off[ru];
+    const uint32_t dout = uint32_t(rdag_off[ru + 1] - wr0);
+    const bool shortl = dout <= 32;
+    uint32_t got = 0;
+    for (uint64_t p0 = b; p0 < e && got < dout; p0 += 32) {
+      const uint64_t p = p0 + lane;
       uint32_t v = 0, rv = 0;
       bool out = false;
       if (p < e) {
@@ -64,17 +89,121 @@ __global__ void fill_kernel(const uint64_t* __restrict__ off, const uint32_t* __
         rv = rank[v];
         out = rv > ru;
       }
-      unsigned ball = __ballot_sync(0xffffffffu, out);
+      const unsigned ball = __ballot_sync(0xffffffffu, out);
       if (out) {
-        uint32_t at = __popc(ball & ((1u << lane) - 1));
+        const uint32_t at = got + __popc(ball & ((1u << lane) - 1));
         if (dag_adj) dag_adj[wid + at] = v;
-        rdag_adj[wr + at] = rv;
+        if (shortl)
+          buf[wib][at] = rv;
+        else
+          rdag_adj[wr0 + at] = rv;
       }
-      wid += __popc(ball);
-      wr += __popc(ball);
+      got += __popc(ball);
+    }
+    if (shortl) {
+      if (dout) {
+        __syncwarp();
+        uint32_t x = lane < dout ? buf[wib][lane] : 0xffffffffu;
+        x = warp_bitonic_sort(x, lane);
+        if (lane < dout) rdag_adj[wr0 + lane] = x;
+      }
+      __syncwarp();
+    } else if (lane == 0) {
+      // mid slices from the front of long_list, longer ones from the back
+      if (dout <= kMidSortL)
+        long_list[atomicAdd(&nlong[0], 1u)] = ru;
+      else
+        long_list[n - 1 - atomicAdd(&nlong[1], 1u)] = ru;
     }
   }
 }
+
+// Bitonic sort of a[0..np2) in shared memory by `nthreads` cooperating
+// threads (index t); the caller synchronises between stages via `sync`.
+template <class Sync>
+__device__ __forceinline__ void smem_bitonic(uint32_t* a, uint32_t np2, uint32_t t,
+                                             uint32_t nthreads, Sync sync) {
+  for (uint32_t k = 2; k <= np2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = t; i < np2; i += nthreads) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint32_t x = a[i], y = a[l];
+          if ((x > y) == ((i & k) == 0)) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      sync();
+    }
+}
+
+constexpr uint32_t kMidSort = 256, kBigSort = 8192;
+
+// Relabelled slices of 33..256 targets: one warp each, in per-warp smem.
+__global__ void __launch_bounds__(256)
+    sort_mid_kernel(const uint32_t* __restrict__ list, uint32_t nl,
+                    const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
+  __shared__ uint32_t sm[8][kMidSort];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl;
+       li += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = list[li];
+    const uint64_t b = off[r];
+    const uint32_t len = uint32_t(off[r + 1] - b);
+    uint32_t np2 = 64;
+    while (np2 < len) np2 <<= 1;
+    uint32_t* a = sm[wib];
+    for (uint32_t i = lane; i < np2; i += 32) a[i] = i < len ? adj[b + i] : 0xffffffffu;
+    __syncwarp();
+    smem_bitonic(a, np2, lane, 32, [] __device__() { __syncwarp(); });
+    for (uint32_t i = lane; i < len; i += 32) adj[b + i] = a[i];
+    __syncwarp();
+  }
+}
+
+// Slices of 257..8192 targets: one CTA each.
+__global__ void __launch_bounds__(512)
+    sort_big_kernel(const uint32_t* __restrict__ list, uint32_t nl,
+                    const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
+  __shared__ uint32_t sm[kBigSort];
+  for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
+    const uint32_t r = list[li];
+    const uint64_t b = off[r];
+    const uint32_t len = uint32_t(off[r + 1] - b);
+    uint32_t np2 = 512;
+    while (np2 < len) np2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
+      sm[i] = i < len ? adj[b + i] : 0xffffffffu;
+    __syncthreads();
+    smem_bitonic(sm, np2, threadIdx.x, blockDim.x, [] __device__() { __syncthreads(); });
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) adj[b + i] = sm[i];
+    __syncthreads();
+  }
+}
+
+// Copies the listed slices from the sort output back into rdag_adj.
+__global__ void copy_slices_kernel(const uint32_t* __restrict__ list, uint32_t nl,
+                                   const uint64_t* __restrict__ off,
+                                   const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+  for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
+    const uint32_t r = list[li];
+    for (uint64_t p = off[r] + threadIdx.x; p < off[r + 1]; p += blockDim.x) dst[p] = src[p];
+  }
+}
+
+// Offsets of the listed (long) relabelled slices, for CUB.
+struct SliceBegin {
+  const uint32_t* list;
+  const uint64_t* off;
+  __host__ __device__ uint64_t operator()(uint32_t i) const { return off[list[i]]; }
+};
+struct SliceEnd {
+  const uint32_t* list;
+  const uint64_t* off;
+  __host__ __device__ uint64_t operator()(uint32_t i) const { return off[list[i] + 1]; }
+};
 
 // Relabel an adopted id-space DAG: slice of u becomes slice rank[u] with
 // targets mapped to ranks; flags edges that do not point up in rank.
@@ -111,17 +240,20 @@ void exclusive_scan_u64(Graph& g, uint64_t* in, uint64_t* out, size_t count) {
   KCG_CUDA(cub::DeviceScan::ExclusiveSum(cub_temp(g, tb), tb, in, out, count, g.stream));
 }
 
-void sort_rdag_and_max(Graph& g, const uint64_t* rdeg) {
-  const uint32_t n = g.n;
-  // max out-degree
-  uint64_t* mx = reinterpret_cast<uint64_t*>(g.counters.ensure(4, &g.bytes));
+void max_out_degree(Graph& g, const uint64_t* rdeg) {
+  uint64_t* mx = reinterpret_cast<uint64_t*>(g.counters.ensure(4, &g.alloc));
   size_t tb = 0;
-  KCG_CUDA(cub::DeviceReduce::Max(nullptr, tb, rdeg, mx, n, g.stream));
-  KCG_CUDA(cub::DeviceReduce::Max(cub_temp(g, tb), tb, rdeg, mx, n, g.stream));
+  KCG_CUDA(cub::DeviceReduce::Max(nullptr, tb, rdeg, mx, g.n, g.stream));
+  KCG_CUDA(cub::DeviceReduce::Max(cub_temp(g, tb), tb, rdeg, mx, g.n, g.stream));
   KCG_CUDA(cudaMemcpyAsync(&g.max_out, mx, 8, cudaMemcpyDeviceToHost, g.stream));
-  // ascending-rank slices
+}
+
+// ascending-rank slices for every vertex (CUB segmented sort)
+void sort_all_slices(Graph& g) {
+  const uint32_t n = g.n;
+  size_t tb = 0;
   if (g.m) {
-    uint32_t* tmp = reinterpret_cast<uint32_t*>(g.scratch2.ensure(g.m * 4 + 16, &g.bytes));
+    uint32_t* tmp = reinterpret_cast<uint32_t*>(g.scratch2.ensure(g.m * 4 + 16, &g.alloc));
     tb = 0;
     KCG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, g.rdag_adj.p, tmp, g.m, n,
                                                 g.rdag_off.p, g.rdag_off.p + 1, g.stream));
@@ -129,7 +261,6 @@ void sort_rdag_and_max(Graph& g, const uint64_t* rdeg) {
                                                 n, g.rdag_off.p, g.rdag_off.p + 1, g.stream));
     KCG_CUDA(cudaMemcpyAsync(g.rdag_adj.p, tmp, g.m * 4, cudaMemcpyDeviceToDevice, g.stream));
   }
-  g.sync();
 }
 
 }  // namespace
@@ -138,15 +269,15 @@ void build_dag(Graph& g, bool want_id_dag) {
   if (!g.has_und) fail(KCG_EINVAL, "handle holds no undirected graph");
   const uint32_t n = g.n;
   g.mark(2);
-  g.rdag_off.ensure(size_t(n) + 1, &g.bytes);
-  g.rdag_adj.ensure(g.m, &g.bytes);
+  g.rdag_off.ensure(size_t(n) + 1, &g.alloc);
+  g.rdag_adj.ensure(g.m, &g.alloc);
   if (want_id_dag) {
-    g.dag_off.ensure(size_t(n) + 1, &g.bytes);
-    g.dag_adj.ensure(g.m, &g.bytes);
+    g.dag_off.ensure(size_t(n) + 1, &g.alloc);
+    g.dag_adj.ensure(g.m, &g.alloc);
   }
   // degree arrays live in pv_rank / pv (n+1 u64 each) until counting
-  uint64_t* rdeg = g.pv_rank.ensure(size_t(n) + 1, &g.bytes);
-  uint64_t* odeg = want_id_dag ? g.pv.ensure(size_t(n) + 1, &g.bytes) : nullptr;
+  uint64_t* rdeg = g.pv_rank.ensure(size_t(n) + 1, &g.alloc);
+  uint64_t* odeg = want_id_dag ? g.pv.ensure(size_t(n) + 1, &g.alloc) : nullptr;
   KCG_CUDA(cudaMemsetAsync(rdeg + n, 0, 8, g.stream));
   if (odeg) KCG_CUDA(cudaMemsetAsync(odeg + n, 0, 8, g.stream));
   unsigned grid = blocks_for(uint64_t(n) * 32, kThreads, 148u * 64u);
@@ -155,13 +286,47 @@ void build_dag(Graph& g, bool want_id_dag) {
   KCG_LAUNCHED(g);
   exclusive_scan_u64(g, rdeg, g.rdag_off.p, size_t(n) + 1);
   if (odeg) exclusive_scan_u64(g, odeg, g.dag_off.p, size_t(n) + 1);
+  uint32_t* lists = reinterpret_cast<uint32_t*>(g.scratch3.ensure(size_t(n) * 4 + 64, &g.alloc));
+  unsigned* cnt = reinterpret_cast<unsigned*>(g.counters.ensure(4, &g.alloc) + 3);
+  KCG_CUDA(cudaMemsetAsync(cnt, 0, 8, g.stream));
   if (n)
     fill_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n,
                                                  want_id_dag ? g.dag_off.p : nullptr,
                                                  want_id_dag ? g.dag_adj.p : nullptr,
-                                                 g.rdag_off.p, g.rdag_adj.p);
+                                                 g.rdag_off.p, g.rdag_adj.p, lists, cnt);
   KCG_LAUNCHED(g);
-  sort_rdag_and_max(g, rdeg);
+  max_out_degree(g, rdeg);
+  unsigned hcnt[2] = {0, 0};
+  KCG_CUDA(cudaMemcpyAsync(hcnt, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
+  g.sync();
+  if (hcnt[0]) {  // 33..256 targets: a warp per slice
+    sort_mid_kernel<<<std::min<unsigned>((hcnt[0] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
+        lists, hcnt[0], g.rdag_off.p, g.rdag_adj.p);
+    KCG_LAUNCHED(g);
+  }
+  if (hcnt[1]) {  // longer slices, listed from the back of `lists`
+    const uint32_t* big = lists + n - hcnt[1];
+    uint32_t maxlen = uint32_t(std::min<uint64_t>(g.max_out, 0xffffffffu));
+    if (maxlen <= kBigSort) {
+      sort_big_kernel<<<std::min<unsigned>(hcnt[1], 148u * 4u), 512, 0, g.stream>>>(
+          big, hcnt[1], g.rdag_off.p, g.rdag_adj.p);
+      KCG_LAUNCHED(g);
+    } else {
+      // CUB segmented sort over just those slices
+      auto cnt_it = thrust::counting_iterator<uint32_t>(0);
+      auto beg = thrust::make_transform_iterator(cnt_it, SliceBegin{big, g.rdag_off.p});
+      auto end = thrust::make_transform_iterator(cnt_it, SliceEnd{big, g.rdag_off.p});
+      uint32_t* tmp = reinterpret_cast<uint32_t*>(g.scratch2.ensure(g.m * 4 + 16, &g.alloc));
+      size_t tb = 0;
+      KCG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, g.rdag_adj.p, tmp, g.m, hcnt[1],
+                                                  beg, end, g.stream));
+      KCG_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_temp(g, tb), tb, g.rdag_adj.p, tmp, g.m,
+                                                  hcnt[1], beg, end, g.stream));
+      copy_slices_kernel<<<std::min<unsigned>(hcnt[1], 148u * 8u), 256, 0, g.stream>>>(
+          big, hcnt[1], g.rdag_off.p, tmp, g.rdag_adj.p);
+      KCG_LAUNCHED(g);
+    }
+  }
   g.mark(3);
   g.times.direct_ms = g.elapsed(2, 3);
   g.has_rdag = true;
@@ -171,16 +336,16 @@ void build_dag(Graph& g, bool want_id_dag) {
 void relabel_from_dag(Graph& g) {
   const uint32_t n = g.n;
   g.mark(2);
-  g.rdag_off.ensure(size_t(n) + 1, &g.bytes);
-  g.rdag_adj.ensure(g.m, &g.bytes);
-  uint64_t* rdeg = g.pv_rank.ensure(size_t(n) + 1, &g.bytes);
+  g.rdag_off.ensure(size_t(n) + 1, &g.alloc);
+  g.rdag_adj.ensure(g.m, &g.alloc);
+  uint64_t* rdeg = g.pv_rank.ensure(size_t(n) + 1, &g.alloc);
   KCG_CUDA(cudaMemsetAsync(rdeg + n, 0, 8, g.stream));
   if (n)
     dag_deg_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(g.dag_off.p, g.rank.p, n,
                                                                        rdeg);
   KCG_LAUNCHED(g);
   exclusive_scan_u64(g, rdeg, g.rdag_off.p, size_t(n) + 1);
-  unsigned long long* bad = g.counters.ensure(4, &g.bytes) + 2;
+  unsigned long long* bad = g.counters.ensure(4, &g.alloc) + 2;
   KCG_CUDA(cudaMemsetAsync(bad, 0, 8, g.stream));
   if (n)
     relabel_kernel<<<blocks_for(uint64_t(n) * 32, kThreads, 148u * 64u), kThreads, 0, g.stream>>>(
@@ -188,7 +353,9 @@ void relabel_from_dag(Graph& g) {
   KCG_LAUNCHED(g);
   unsigned long long nbad = 0;
   KCG_CUDA(cudaMemcpyAsync(&nbad, bad, 8, cudaMemcpyDeviceToHost, g.stream));
-  sort_rdag_and_max(g, rdeg);
+  max_out_degree(g, rdeg);
+  sort_all_slices(g);
+  g.sync();
   if (nbad) fail(KCG_EINVAL, "DAG edge does not point toward higher rank");
   g.mark(3);
   g.times.direct_ms = g.elapsed(2, 3);

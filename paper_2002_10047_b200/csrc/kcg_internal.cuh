@@ -41,33 +41,43 @@ void set_last_error(const std::string& msg);
   } while (0)
 
 // ---- device buffers ----------------------------------------------------------
+// Stream-ordered allocations from the device's default memory pool (release
+// threshold raised at init), so creating and destroying handles -- the
+// end-to-end path of every drop-in call -- reuses memory instead of paying
+// cudaMalloc/cudaFree each time.
+struct AllocCtx {
+  size_t bytes = 0;             // device bytes the handle holds
+  cudaStream_t stream = nullptr;
+};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
-  size_t n = 0;     // elements allocated
-  size_t* acct = nullptr;  // byte accounting of the owning handle
+  size_t n = 0;           // elements allocated
+  AllocCtx* ctx = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
     if (p) {
-      cudaFree(p);
-      if (acct) *acct -= n * sizeof(T);
+      cudaFreeAsync(p, ctx ? ctx->stream : nullptr);
+      if (ctx) ctx->bytes -= n * sizeof(T);
     }
     p = nullptr;
     n = 0;
   }
   // grows (never shrinks) to at least `count` elements; contents are lost
   // when it grows
-  T* ensure(size_t count, size_t* account = nullptr) {
-    if (account) acct = account;
+  T* ensure(size_t count, AllocCtx* c = nullptr) {
+    if (c) ctx = c;
     if (count <= n && p) return p;
     release();
-    size_t c = count ? count : 1;
-    KCG_CUDA(cudaMalloc(&p, c * sizeof(T)));
-    n = c;
-    if (acct) *acct += n * sizeof(T);
+    const size_t e = count ? count : 1;
+    KCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), e * sizeof(T),
+                             ctx ? ctx->stream : nullptr));
+    n = e;
+    if (ctx) ctx->bytes += n * sizeof(T);
     return p;
   }
 };
@@ -115,7 +125,7 @@ struct Graph {
   bool has_dag = false;     // id-space DAG valid for current ranking
   bool has_rdag = false;    // relabelled DAG valid for current ranking
   uint64_t max_out = 0;
-  size_t bytes = 0;
+  AllocCtx alloc;
   cudaStream_t stream = nullptr;
 
   DevBuf<uint64_t> und_off;
@@ -146,6 +156,7 @@ struct Graph {
 
   Graph();
   ~Graph();
+  void release_all();
   void sync();
   // event-timed region on the handle's stream
   void mark(int i) { KCG_CUDA(cudaEventRecord(ev[i], stream)); }

@@ -248,7 +248,7 @@ Peel peel_state(Graph& g, bool with_keys) {
   size_t o_wdeg = carve(n * 4), o_alive = carve(n), o_rem = carve(n * 4),
          o_rem2 = carve(n * 4), o_batch = carve(n * 4), o_pos = carve(n * 4 + 4);
   size_t o_keys = with_keys ? carve(n * 8) : 0, o_keys2 = with_keys ? carve(n * 8) : 0;
-  unsigned char* base = g.scratch2.ensure(bytes + 256, &g.bytes);
+  unsigned char* base = g.scratch2.ensure(bytes + 256, &g.alloc);
   Peel p;
   p.wdeg = reinterpret_cast<uint32_t*>(base + o_wdeg);
   p.alive = base + o_alive;
@@ -258,7 +258,7 @@ Peel peel_state(Graph& g, bool with_keys) {
   p.pos = reinterpret_cast<uint32_t*>(base + o_pos);
   p.keys = with_keys ? reinterpret_cast<uint64_t*>(base + o_keys) : nullptr;
   p.keys2 = with_keys ? reinterpret_cast<uint64_t*>(base + o_keys2) : nullptr;
-  p.ctr = g.counters.ensure(8, &g.bytes);
+  p.ctr = g.counters.ensure(8, &g.alloc);
   if (n) {
     KCG_CUDA(cudaMemcpyAsync(p.wdeg, g.deg.p, n * 4, cudaMemcpyDeviceToDevice, g.stream));
     KCG_CUDA(cudaMemsetAsync(p.alive, 1, n, g.stream));
@@ -296,7 +296,7 @@ void rank_degree(Graph& g) {
   // stable LSD radix sort of ids keyed by degree == std::stable_sort by
   // degree (orientation.cpp:10-17)
   size_t off_vals = (size_t(n) * 4 + 255) & ~size_t(255);
-  unsigned char* base = g.scratch2.ensure(off_vals * 3 + 256, &g.bytes);
+  unsigned char* base = g.scratch2.ensure(off_vals * 3 + 256, &g.alloc);
   uint32_t* vals_in = reinterpret_cast<uint32_t*>(base);
   uint32_t* keys_out = reinterpret_cast<uint32_t*>(base + off_vals);
   uint32_t* maxd = reinterpret_cast<uint32_t*>(base + 2 * off_vals);
@@ -309,7 +309,7 @@ void rank_degree(Graph& g) {
   KCG_CUDA(cudaMemcpyAsync(&mx, maxd, 4, cudaMemcpyDeviceToHost, g.stream));
   g.sync();
   int end_bit = std::max(1, bits_for(mx));
-  g.order.ensure(n, &g.bytes);
+  g.order.ensure(n, &g.alloc);
   tb = 0;
   KCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, g.deg.p, keys_out, vals_in, g.order.p,
                                            n, 0, end_bit, g.stream));
@@ -523,7 +523,7 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
     fail(KCG_EINVAL, "unknown orientation strategy");
   if ((strategy == KCG_BARENBOIM_ELKIN || strategy == KCG_GOODRICH_PSZONA) && !(eps > 0))
     fail(KCG_EINVAL, "epsilon must be positive");
-  g.rank.ensure(g.n, &g.bytes);
+  g.rank.ensure(g.n, &g.alloc);
   g.mark(2);
   uint64_t rounds = 0;
   switch (strategy) {
@@ -548,7 +548,7 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
     }
   }
   // order[] (inverse permutation) for the relabelled DAG
-  g.order.ensure(g.n, &g.bytes);
+  g.order.ensure(g.n, &g.alloc);
   if (g.n && strategy != KCG_DEGREE) {
     invert_kernel<<<blocks_for(g.n, kThreads), kThreads, 0, g.stream>>>(g.rank.p, g.n, g.order.p);
     KCG_LAUNCHED(g);
