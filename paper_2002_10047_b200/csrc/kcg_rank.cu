@@ -7,6 +7,7 @@
 // Within a round the rank order is the id order, produced by an ordered
 // exclusive scan over the id-sorted remaining list (never by atomic
 // arrival order).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -387,87 +388,142 @@ uint64_t rank_gp(Graph& g, double eps) {
   return rounds;
 }
 
-uint64_t rank_kcore(Graph& g) {
-  // Parallel bucketed degeneracy peel: every alive vertex
-  // whose induced degree is <= level leaves in the same round, ranked by
-  // (round, id); level only rises when the frontier empties.  Max
-  // out-degree equals the degeneracy, like the sequential heap of
-  // orientation.cpp:23-46, but the order itself differs (documented
-  // deviation in DESIGN.md).
-  const uint32_t n = g.n;
-  Peel P = peel_state(g, true);
-  uint32_t* front = P.batch;
-  uint32_t* next = P.pos;
-  uint32_t* sorted = reinterpret_cast<uint32_t*>(P.keys2);
-  uint32_t nrem = n, placed = 0, level = 0;
-  uint64_t rounds = 0;
-  unsigned long long* ctr = P.ctr;
-  uint32_t* minbuf = reinterpret_cast<uint32_t*>(P.keys);
+// Degeneracy peel in one cooperative kernel: every alive vertex whose
+// induced degree is <= level leaves in the same round; level only rises
+// when the frontier empties.  Each vertex records its removal round; ranks
+// are the (round, id) order, assigned afterwards by one radix sort.  Grid-
+// wide syncs replace the per-round host round trips.
+struct KcoreArgs {
+  const uint64_t* off;
+  const uint32_t* adj;
+  uint32_t n;
+  uint32_t* deg;     // working induced degrees
+  uint32_t* rnd;     // removal round, 0xffffffff while alive
+  uint32_t* front;   // two frontier buffers of n entries
+  unsigned* ctr;     // [0],[1] frontier sizes, [2] min degree, [3] rounds, [4] level
+};
+
+__global__ void __launch_bounds__(256) kcore_coop_kernel(KcoreArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t n = a.n;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gwarp = tid >> 5, nwarps = nthreads >> 5;
+  uint32_t level = 0, round = 0, placed = 0, cur = 0;
+  uint32_t* fr[2] = {a.front, a.front + n};
   while (placed < n) {
-    // level change: compact the alive remaining list, take its min degree
-    {
-      size_t tb = 0;
-      // select alive ids from rem (stable)
-      AliveSel sel{P.alive};
-      KCG_CUDA(cub::DeviceSelect::If(nullptr, tb, P.rem, P.rem2,
-                                     reinterpret_cast<uint32_t*>(ctr), nrem, sel, g.stream));
-      KCG_CUDA(cub::DeviceSelect::If(cub_temp(g, tb), tb, P.rem, P.rem2,
-                                     reinterpret_cast<uint32_t*>(ctr), nrem, sel, g.stream));
-      uint32_t cnt = 0;
-      KCG_CUDA(cudaMemcpyAsync(&cnt, ctr, 4, cudaMemcpyDeviceToHost, g.stream));
-      g.sync();
-      std::swap(P.rem, P.rem2);
-      nrem = cnt;
-      if (!nrem) break;
-      auto it = thrust::make_transform_iterator(thrust::counting_iterator<uint32_t>(0),
-                                                AliveDeg{P.rem, P.wdeg, P.alive});
-      tb = 0;
-      KCG_CUDA(cub::DeviceReduce::Min(nullptr, tb, it, minbuf, nrem, g.stream));
-      KCG_CUDA(cub::DeviceReduce::Min(cub_temp(g, tb), tb, it, minbuf, nrem, g.stream));
-      uint32_t mn = 0;
-      KCG_CUDA(cudaMemcpyAsync(&mn, minbuf, 4, cudaMemcpyDeviceToHost, g.stream));
-      g.sync();
-      level = std::max(level, mn);
-      // initial frontier for this level, already in id order
-      tb = 0;
-      AtLevel pred{P.rem, P.wdeg, P.alive, level};
-      KCG_CUDA(cub::DeviceSelect::If(nullptr, tb, P.rem, front,
-                                     reinterpret_cast<uint32_t*>(ctr), nrem, pred, g.stream));
-      KCG_CUDA(cub::DeviceSelect::If(cub_temp(g, tb), tb, P.rem, front,
-                                     reinterpret_cast<uint32_t*>(ctr), nrem, pred, g.stream));
-    }
-    uint32_t nf = 0;
-    KCG_CUDA(cudaMemcpyAsync(&nf, ctr, 4, cudaMemcpyDeviceToHost, g.stream));
-    g.sync();
-    bool sorted_already = true;
-    while (nf) {
-      rounds++;
-      uint32_t* f = front;
-      if (!sorted_already) {
-        size_t tb = 0;
-        int end_bit = std::max(1, bits_for(n - 1));
-        KCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, front, sorted, nf, 0, end_bit,
-                                                g.stream));
-        KCG_CUDA(cub::DeviceRadixSort::SortKeys(cub_temp(g, tb), tb, front, sorted, nf, 0,
-                                                end_bit, g.stream));
-        f = sorted;
+    uint32_t nf = a.ctr[cur];
+    if (nf == 0) {
+      // level change: min alive degree, then every alive vertex at or below
+      if (tid == 0) a.ctr[2] = 0xffffffffu;
+      grid.sync();
+      uint32_t mn = 0xffffffffu;
+      for (uint32_t v = tid; v < n; v += nthreads)
+        if (a.rnd[v] == 0xffffffffu) mn = min(mn, a.deg[v]);
+      mn = __reduce_min_sync(0xffffffffu, mn);
+      if (lane == 0 && mn != 0xffffffffu) atomicMin(&a.ctr[2], mn);
+      grid.sync();
+      level = max(level, a.ctr[2]);
+      for (uint32_t v0 = 0; v0 < n; v0 += nthreads) {
+        const uint32_t v = v0 + tid;
+        const bool take = v < n && a.rnd[v] == 0xffffffffu && a.deg[v] <= level;
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&a.ctr[cur], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) fr[cur][base + __popc(bal & ((1u << lane) - 1))] = v;
       }
-      kcore_kill_rank_kernel<<<blocks_for(nf, kThreads), kThreads, 0, g.stream>>>(
-          f, nf, placed, P.alive, g.rank.p);
-      KCG_LAUNCHED(g);
-      KCG_CUDA(cudaMemsetAsync(ctr, 0, 8, g.stream));
-      kcore_decrement_kernel<<<blocks_for(uint64_t(nf) * 32, kThreads), kThreads, 0, g.stream>>>(
-          f, nf, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, level, next, ctr);
-      KCG_LAUNCHED(g);
-      placed += nf;
-      unsigned long long nn = 0;
-      KCG_CUDA(cudaMemcpyAsync(&nn, ctr, 8, cudaMemcpyDeviceToHost, g.stream));
-      g.sync();
-      std::swap(front, next);
-      nf = uint32_t(nn);
-      sorted_already = false;
+      grid.sync();
+      nf = a.ctr[cur];
     }
+    // this round: mark, then decrement survivors and collect the next
+    // frontier (a survivor crossing level+1 -> level joins exactly once)
+    for (uint32_t i = tid; i < nf; i += nthreads) a.rnd[fr[cur][i]] = round;
+    if (tid == 0) a.ctr[cur ^ 1] = 0;
+    grid.sync();
+    for (uint32_t w = gwarp; w < nf; w += nwarps) {
+      const uint32_t v = fr[cur][w];
+      const uint64_t e = a.off[v + 1];
+      for (uint64_t p0 = a.off[v]; p0 < e; p0 += 32) {
+        const uint64_t p = p0 + lane;
+        bool join = false;
+        uint32_t u = 0;
+        if (p < e) {
+          u = a.adj[p];
+          if (a.rnd[u] == 0xffffffffu) join = atomicSub(&a.deg[u], 1u) == level + 1;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, join);
+        if (bal) {
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(&a.ctr[cur ^ 1], __popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (join) fr[cur ^ 1][base + __popc(bal & ((1u << lane) - 1))] = u;
+        }
+      }
+    }
+    placed += nf;
+    round++;
+    if (tid == 0) a.ctr[cur] = 0;
+    grid.sync();
+    cur ^= 1;
   }
+  if (tid == 0) a.ctr[3] = round;
+}
+
+__global__ void kcore_keys_kernel(const uint32_t* __restrict__ rnd, uint32_t n, int idbits,
+                                  uint64_t* __restrict__ keys) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    keys[v] = (uint64_t(rnd[v]) << idbits) | v;
+}
+
+__global__ void kcore_rank_kernel(const uint64_t* __restrict__ sorted, uint32_t n,
+                                  uint64_t idmask, uint32_t* __restrict__ rank,
+                                  uint32_t* __restrict__ order) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = uint32_t(sorted[i] & idmask);
+    rank[v] = i;
+    order[i] = v;
+  }
+}
+
+uint64_t rank_kcore(Graph& g) {
+  // the reference pops one (degree, id) heap minimum at a
+  // time (orientation.cpp:23-46), which is inherently sequential.  This
+  // order differs, its max out-degree (= degeneracy) does not.
+  const uint32_t n = g.n;
+  if (!n) return 0;
+  Peel P = peel_state(g, true);
+  unsigned* ctr = reinterpret_cast<unsigned*>(P.ctr);
+  KCG_CUDA(cudaMemsetAsync(ctr, 0, 8 * 4, g.stream));
+  uint32_t* rnd = P.rem;  // reuse: removal round per vertex
+  KCG_CUDA(cudaMemsetAsync(rnd, 0xff, size_t(n) * 4, g.stream));
+  uint32_t* front = reinterpret_cast<uint32_t*>(P.keys);  // 2n u32 fit in n u64
+  KcoreArgs ka{g.und_off.p, g.und_adj.p, n, P.wdeg, rnd, front, ctr};
+  int occ = 0;
+  KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kcore_coop_kernel, 256, 0));
+  const unsigned grid = unsigned(std::max(1, occ) * device().sms);
+  void* args[] = {&ka};
+  KCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kcore_coop_kernel), grid, 256,
+                                       args, 0, g.stream));
+  KCG_LAUNCHED(g);
+  const int idbits = std::max(1, bits_for(n - 1));
+  kcore_keys_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(rnd, n, idbits, P.keys2);
+  KCG_LAUNCHED(g);
+  uint64_t* sorted = P.keys;
+  size_t tb = 0;
+  const int end_bit = std::min(64, idbits + 32);
+  KCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, P.keys2, sorted, n, 0, end_bit, g.stream));
+  KCG_CUDA(cub::DeviceRadixSort::SortKeys(cub_temp(g, tb), tb, P.keys2, sorted, n, 0, end_bit,
+                                          g.stream));
+  g.order.ensure(n, &g.alloc);
+  kcore_rank_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(
+      sorted, n, (uint64_t(1) << idbits) - 1, g.rank.p, g.order.p);
+  KCG_LAUNCHED(g);
+  unsigned rounds = 0;
+  KCG_CUDA(cudaMemcpyAsync(&rounds, ctr + 3, 4, cudaMemcpyDeviceToHost, g.stream));
+  g.sync();
   return rounds;
 }
 
