@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
         }
       }
     } else if (R == 2) {
-      c = lane_pairs<PV>(lane < d, S.usym[lane], lane, S.usym, sym, cpv);
+      c = lane_pairs<PV>(lane < d, S.usym[lane], lane, S.usym, sym, cpv, lane);
     } else if (R <= 32) {
       if constexpr (MAXL > 0)
         c = steal_count<PV, SL>(lane < d, S.usym[lane], R, lane, S.usym, sym, cpv, *stk, S.map,
@@ -383,9 +383,9 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
   // compact out-neighbourhood, balanced across lanes by the DFS engine
   ull ct = 0;
   if constexpr (MAXL == 0) {
-    ct = lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv);  // R == 3
+    ct = lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv, lane);  // R == 3
   } else {
-    ct = R == 3 ? lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv)
+    ct = R == 3 ? lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv, lane)
                 : steal_count<PV, MAXL>(lane < s, c.cusym[lane], R - 1, lane, c.cusym, c.csym,
                                         c.cpv, *reinterpret_cast<Stacks<PV, MAXL>*>(c.stk),
                                         c.cand, lane);

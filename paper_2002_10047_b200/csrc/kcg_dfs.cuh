@@ -45,22 +45,40 @@ __device__ __forceinline__ void leaf_node_pv(uint32_t N, const uint32_t* sym, ul
 
 constexpr int DFS_STEPS = 8;  // steps between steal checks
 
+// Per-vertex credit of leaf nodes, transposed: every lane that created a
+// leaf node N this step broadcasts it and lane v adds its degree inside N
+// (popc(N ∩ N(v))) to its own register accumulator `acc`.  Called by all
+// 32 lanes.
+__device__ __forceinline__ void leaf_pv_collect(bool made, uint32_t N, uint32_t my_sym,
+                                                uint32_t lane, ull& acc) {
+  unsigned mk = __ballot_sync(0xffffffffu, made);
+  while (mk) {
+    const int c = __ffs(mk) - 1;
+    mk &= mk - 1;
+    const uint32_t Nc = __shfl_sync(0xffffffffu, N, c);
+    if ((Nc >> lane) & 1u) acc += __popc(Nc & my_sym);
+  }
+}
+
 // R == 2 needs no stack: one loop over N per lane (the last two vertices).
+// Must be called by all 32 lanes (PV uses warp collectives).
 template <bool PV>
 __device__ __forceinline__ ull lane_pairs(bool active, uint32_t N, uint32_t root_v,
-                                          const uint32_t* usym, const uint32_t* sym, ull* cpv) {
-  if (!active) return 0;
+                                          const uint32_t* usym, const uint32_t* sym, ull* cpv,
+                                          uint32_t lane) {
   ull t = 0;
-  for (uint32_t b = N; b;) {
-    const int x = __ffs(b) - 1;
-    b &= b - 1;
-    t += __popc(N & usym[x]);
+  if (active) {
+    for (uint32_t b = N; b;) {
+      const int x = __ffs(b) - 1;
+      b &= b - 1;
+      t += __popc(N & usym[x]);
+    }
   }
   if constexpr (PV) {
-    if (t) {
-      leaf_node_pv<PV>(N, sym, cpv);
-      atomicAdd(&cpv[root_v], t);
-    }
+    ull acc = 0;
+    leaf_pv_collect(t != 0, N, sym[lane], lane, acc);
+    if (acc) atomicAdd(&cpv[lane], acc);
+    if (t) atomicAdd(&cpv[root_v], t);
   }
   return t;
 }
@@ -88,17 +106,19 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
   uint32_t smask = 0;       // ancestor levels (< lvl) with >= 2 unchosen
   ull total = 0;
   ull csub = 0;  // PV: subtree count of the current node
+  ull acc = 0;   // PV: leaf credit of compact vertex `lane`
+  const uint32_t my_sym = PV ? sym[lane] : 0u;
   if (active && __popc(N0) >= R) {
     lvl = 0;
     cN = cI = N0;
-    if constexpr (PV) {
-      st.X[0][lane] = root_v;
-      if (R == 2) leaf_node_pv<PV>(N0, sym, cpv);
-    }
+    if constexpr (PV) st.X[0][lane] = root_v;
   }
+  if constexpr (PV) leaf_pv_collect(lvl == 0 && R == 2, N0, my_sym, lane, acc);
   for (;;) {
 #pragma unroll
     for (int t = 0; t < DFS_STEPS; t++) {
+      bool made_leaf = false;
+      uint32_t leafN = 0;
       if (lvl >= base) {
         if (cI == 0) {
           // node exhausted: credit and pop
@@ -133,13 +153,15 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
               st.sub[lvl][lane] = csub;
               csub = 0;
               st.X[lvl + 1][lane] = x;
-              if (r - 1 == 2) leaf_node_pv<PV>(child, sym, cpv);
+              made_leaf = r - 1 == 2;
+              leafN = child;
             }
             lvl++;
             cN = cI = child;
           }
         }
       }
+      if constexpr (PV) leaf_pv_collect(made_leaf, leafN, my_sym, lane, acc);
     }
     const bool busy = lvl >= base;
     const unsigned busym = __ballot_sync(FULLM, busy);
@@ -188,6 +210,9 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
       }
     }
     __syncwarp();
+  }
+  if constexpr (PV) {
+    if (acc) atomicAdd(&cpv[lane], acc);
   }
   return total;
 }
