@@ -94,14 +94,14 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     uint32_t qy[64], qi[64];
   };
   __shared__ WarpSmem s_w[WARP_TIER_WARPS];
-  __shared__ ull s_pv[PV ? WARP_TIER_WARPS : 1][32];
+  __shared__ pvc_t s_pv[PV ? WARP_TIER_WARPS : 1][32];
   extern __shared__ __align__(16) unsigned char dyn_smem[];  // per-warp DFS stacks
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpSmem& S = s_w[wib];
   constexpr int SL = MAXL > 0 ? MAXL : 1;
   Stacks<PV, SL>* stk = reinterpret_cast<Stacks<PV, SL>*>(dyn_smem) + wib;
   uint32_t* sym = S.sym;
-  ull* cpv = s_pv[PV ? wib : 0];
+  pvc_t* cpv = s_pv[PV ? wib : 0];
   const Member M{S.table, S.filter, 6, 9};
   const int R = k - 2;
   ull my_total = 0, my_staged = 0;
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
       if (lane < d) {
         c = __popc(S.usym[lane]);
         if constexpr (PV) {
-          for (uint32_t bb = S.usym[lane]; bb; bb &= bb - 1) atomicAdd(&cpv[__ffs(bb) - 1], 1ull);
-          if (c) atomicAdd(&cpv[lane], c);
+          for (uint32_t bb = S.usym[lane]; bb; bb &= bb - 1) atomicAdd(&cpv[__ffs(bb) - 1], 1u);
+          if (c) atomicAdd(&cpv[lane], pvc_t(c));
         }
       }
     } else if (R == 2) {
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     if constexpr (PV) {
       __syncwarp();
       ull src_total = warp_sum(c);
-      if (lane < d && cpv[lane]) atomicAdd(&pv_rank[w], cpv[lane]);
+      if (lane < d && cpv[lane]) atomicAdd(&pv_rank[w], ull(cpv[lane]));
       if (lane == 0 && src_total) atomicAdd(&pv_rank[u], src_total);
     }
     __syncwarp();
@@ -320,7 +320,7 @@ struct WarpCtx {
   uint32_t* cusym;      // 32 words: compact rows, upper part
   void* stk;            // Stacks<PV, MAXL> of the warp's DFS engine
   uint32_t* qy;         // 128 words: staging queue (keys, rows)
-  ull* cpv;             // 32 (PV)
+  pvc_t* cpv;           // 32 (PV)
   ull* pvl;             // d (PV)
   Lvl* lvl;
   uint32_t lane;
@@ -392,7 +392,7 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
   }
   __syncwarp();
   if constexpr (PV) {
-    if (lane < s && c.cpv[lane]) atomicAdd(&c.pvl[xt], c.cpv[lane]);
+    if (lane < s && c.cpv[lane]) atomicAdd(&c.pvl[xt], ull(c.cpv[lane]));
   }
   ull tot = warp_sum(ct);
   __syncwarp();
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
   c.cusym = reinterpret_cast<uint32_t*>(wbase + L.w_cusym);
   c.stk = wbase + L.w_stk;
   c.qy = reinterpret_cast<uint32_t*>(wbase + L.w_q);
-  c.cpv = reinterpret_cast<ull*>(wbase + L.w_cpv);
+  c.cpv = reinterpret_cast<pvc_t*>(wbase + L.w_cpv);
   c.lvl = reinterpret_cast<Lvl*>(wbase + L.w_lvl);
   c.pvl = pvl;
   c.lane = lane;

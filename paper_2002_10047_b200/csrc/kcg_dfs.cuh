@@ -34,14 +34,10 @@ struct Stacks {
   ull sub[PV ? MAXL : 1][32];         // subtree counts per level
 };
 
-template <bool PV>
-__device__ __forceinline__ void leaf_node_pv(uint32_t N, const uint32_t* sym, ull* cpv) {
-  for (uint32_t b = N; b; b &= b - 1) {
-    const int v = __ffs(b) - 1;
-    const uint32_t c = __popc(N & sym[v]);
-    if (c) atomicAdd(&cpv[v], ull(c));
-  }
-}
+// Compact-problem per-vertex counters are 32-bit: within one problem of
+// <= 32 vertices a vertex lies in at most C(31,15) < 2^32 cliques, and the
+// counters are flushed to 64-bit per problem.
+typedef uint32_t pvc_t;
 
 constexpr int DFS_STEPS = 8;  // steps between steal checks
 
@@ -50,7 +46,7 @@ constexpr int DFS_STEPS = 8;  // steps between steal checks
 // (popc(N ∩ N(v))) to its own register accumulator `acc`.  Called by all
 // 32 lanes.
 __device__ __forceinline__ void leaf_pv_collect(bool made, uint32_t N, uint32_t my_sym,
-                                                uint32_t lane, ull& acc) {
+                                                uint32_t lane, pvc_t& acc) {
   unsigned mk = __ballot_sync(0xffffffffu, made);
   while (mk) {
     const int c = __ffs(mk) - 1;
@@ -64,7 +60,7 @@ __device__ __forceinline__ void leaf_pv_collect(bool made, uint32_t N, uint32_t 
 // Must be called by all 32 lanes (PV uses warp collectives).
 template <bool PV>
 __device__ __forceinline__ ull lane_pairs(bool active, uint32_t N, uint32_t root_v,
-                                          const uint32_t* usym, const uint32_t* sym, ull* cpv,
+                                          const uint32_t* usym, const uint32_t* sym, pvc_t* cpv,
                                           uint32_t lane) {
   ull t = 0;
   if (active) {
@@ -75,10 +71,10 @@ __device__ __forceinline__ ull lane_pairs(bool active, uint32_t N, uint32_t root
     }
   }
   if constexpr (PV) {
-    ull acc = 0;
+    pvc_t acc = 0;
     leaf_pv_collect(t != 0, N, sym[lane], lane, acc);
     if (acc) atomicAdd(&cpv[lane], acc);
-    if (t) atomicAdd(&cpv[root_v], t);
+    if (t) atomicAdd(&cpv[root_v], pvc_t(t));
   }
   return t;
 }
@@ -97,7 +93,7 @@ __device__ __forceinline__ uint32_t upper_split(uint32_t I) {
 // is 32 words of warp-private shared memory.
 template <bool PV, int MAXL>
 __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
-                           const uint32_t* usym, const uint32_t* sym, ull* cpv,
+                           const uint32_t* usym, const uint32_t* sym, pvc_t* cpv,
                            Stacks<PV, MAXL>& st, uint32_t* map, uint32_t lane) {
   constexpr uint32_t FULLM = 0xffffffffu;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -106,7 +102,7 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
   uint32_t smask = 0;       // ancestor levels (< lvl) with >= 2 unchosen
   ull total = 0;
   ull csub = 0;  // PV: subtree count of the current node
-  ull acc = 0;   // PV: leaf credit of compact vertex `lane`
+  pvc_t acc = 0;  // PV: leaf credit of compact vertex `lane`
   const uint32_t my_sym = PV ? sym[lane] : 0u;
   if (active && __popc(N0) >= R) {
     lvl = 0;
@@ -124,10 +120,10 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
           // node exhausted: credit and pop
           if constexpr (PV) {
             if (lvl > base) {
-              if (csub) atomicAdd(&cpv[st.X[lvl][lane]], csub);
+              if (csub) atomicAdd(&cpv[st.X[lvl][lane]], pvc_t(csub));
               csub += st.sub[lvl - 1][lane];
             } else if (csub) {
-              for (int l = 0; l <= base; l++) atomicAdd(&cpv[st.X[l][lane]], csub);
+              for (int l = 0; l <= base; l++) atomicAdd(&cpv[st.X[l][lane]], pvc_t(csub));
             }
           }
           if (lvl > base) {
