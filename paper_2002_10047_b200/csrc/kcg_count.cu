@@ -263,11 +263,16 @@ struct Layout {
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Bitmap row stride in words: a multiple of 4 (rows are read with 128-bit
+// shared loads) with an odd number of 16-byte units, so lanes reading
+// different rows at the same offset spread over the banks.
+__host__ __device__ inline uint32_t row_stride(uint32_t W) { return 4u * (((W + 3u) >> 2) | 1u); }
+
 __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bool pv, int nw,
                                               size_t stk_bytes) {
   Layout L;
   L.dmax = dmax;
-  L.wpmax = ((dmax + 31) / 32) | 1u;
+  L.wpmax = row_stride((dmax + 31) / 32);
   uint32_t tb = 6;
   while ((1u << tb) < 2 * dmax) tb++;
   L.tbits = tb;
@@ -594,7 +599,7 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
     const uint32_t slice = a.item_sl[si] >> 16, nsl = a.item_sl[si] & 0xffffu;
     const uint64_t b = a.off[u];
     const uint32_t d = uint32_t(a.off[u + 1] - b);
-    const uint32_t W = (d + 31) / 32, wp = W | 1u;
+    const uint32_t W = (d + 31) / 32, wp = row_stride(W);
     uint32_t tb = 6;
     while ((1u << tb) < 2 * d) tb++;
     const uint32_t fb = tb + 4 > 14 ? (tb + 4 > 20 ? 20 : tb + 4) : 14;
@@ -683,8 +688,22 @@ __global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
           const uint32_t x = 32 * w + __ffs(bits) - 1;
           bits &= bits - 1;
           const uint32_t* rx = sym + size_t(x) * wp;
-          uint32_t cx = __popc(ri[w] & rx[w] & above_mask(x & 31));
-          for (uint32_t w2 = w + 1; w2 < W; w2++) cx += __popc(ri[w2] & rx[w2]);
+          // |row_i ∩ row_x| above x, 4 words per 128-bit load
+          const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
+          const uint4* rx4 = reinterpret_cast<const uint4*>(rx);
+          const uint32_t g0 = w >> 2, G = (W + 3) >> 2, ax = above_mask(x & 31);
+          uint4 va = ri4[g0], vb = rx4[g0];
+          const uint32_t b0 = g0 * 4;
+          uint32_t cx = __popc(va.x & vb.x & (b0 < w ? 0u : (b0 == w ? ax : FULL))) +
+                        __popc(va.y & vb.y & (b0 + 1 < w ? 0u : (b0 + 1 == w ? ax : FULL))) +
+                        __popc(va.z & vb.z & (b0 + 2 < w ? 0u : (b0 + 2 == w ? ax : FULL))) +
+                        __popc(va.w & vb.w & (b0 + 3 < w ? 0u : (b0 + 3 == w ? ax : FULL)));
+          for (uint32_t g = g0 + 1; g < G; g++) {
+            va = ri4[g];
+            vb = rx4[g];
+            cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
+                  __popc(va.w & vb.w);
+          }
           ci += cx;
           if constexpr (PV) {
             // x's degree inside N+(u) ∩ N+(i): also counts the 4th-vertex role
