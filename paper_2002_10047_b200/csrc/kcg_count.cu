@@ -345,24 +345,26 @@ __device__ ull set_members_pv(const WarpCtx& c, const uint32_t* S) {
   return warp_sum(cnt);
 }
 
-// Writes the members of S (ascending) into c.cand; returns their number.
+// Writes the first `limit` (<= 64) members of S (ascending) into c.cand,
+// one word per step with lane j taking bit j; returns their number.
 __device__ uint32_t enumerate_members(const WarpCtx& c, const uint32_t* S, uint32_t limit) {
-  uint32_t base = 0;
-  for (uint32_t w0 = 0; w0 < c.W && base < limit; w0 += 32) {
-    uint32_t w = w0 + c.lane;
-    uint32_t v = w < c.W ? S[w] : 0u;
-    uint32_t n = __popc(v);
-    uint32_t incl = n;
-    for (int s = 1; s < 32; s <<= 1) {
-      uint32_t t = __shfl_up_sync(FULL, incl, s);
-      if (c.lane >= uint32_t(s)) incl += t;
+  uint32_t qn = 0;
+  const uint32_t lane = c.lane, lt = (1u << lane) - 1u;
+  for (uint32_t w0 = 0; w0 < c.W && qn < limit; w0 += 32) {
+    const uint32_t wl = w0 + lane;
+    const uint32_t mine = wl < c.W ? S[wl] : 0u;
+    uint32_t nz = __ballot_sync(FULL, mine != 0);
+    while (nz && qn < limit) {
+      const uint32_t j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t v = __shfl_sync(FULL, mine, j);
+      const uint32_t pos = qn + __popc(v & lt);
+      if (((v >> lane) & 1u) && pos < limit) c.cand[pos] = 32 * (w0 + j) + lane;
+      qn += __popc(v);
     }
-    uint32_t pos = base + incl - n;
-    for (; v && pos < limit; v &= v - 1) c.cand[pos++] = 32 * w + __ffs(v) - 1;
-    base += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
-  return base < limit ? base : limit;
+  return qn < limit ? qn : limit;
 }
 
 // |S| <= 32: transpose S's induced rows into one word per member (ballot),
@@ -404,44 +406,70 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
   return tot;
 }
 
-// R == 2: sum over members x of |S ∩ N+(x)|, one member per lane, each
-// lane running its member's multi-word dot product.  Members are gathered
-// 32 at a time into the warp's 32-entry candidate buffer.
+// |S ∩ N+(x)| above x for member x of S (128-bit loads; the bitmap's row
+// padding is zero, so S's padding words never count).
+template <bool PV>
+__device__ __forceinline__ void dot_member(const WarpCtx& c, const uint32_t* S, uint32_t x,
+                                           ull& cnt) {
+  const uint32_t* row = c.sym + size_t(x) * c.wp;
+  const uint4* S4 = reinterpret_cast<const uint4*>(S);
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  const uint32_t xw = x >> 5, g0 = xw >> 2, b0 = g0 * 4, G = (c.W + 3) >> 2;
+  const uint32_t ax = above_mask(x & 31);
+  uint4 va = S4[g0], vb = r4[g0];
+  uint32_t acc = __popc(va.x & vb.x & (b0 < xw ? 0u : (b0 == xw ? ax : FULL))) +
+                 __popc(va.y & vb.y & (b0 + 1 < xw ? 0u : (b0 + 1 == xw ? ax : FULL))) +
+                 __popc(va.z & vb.z & (b0 + 2 < xw ? 0u : (b0 + 2 == xw ? ax : FULL))) +
+                 __popc(va.w & vb.w & (b0 + 3 < xw ? 0u : (b0 + 3 == xw ? ax : FULL)));
+  for (uint32_t g = g0 + 1; g < G; g++) {
+    va = S4[g];
+    vb = r4[g];
+    acc += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) + __popc(va.w & vb.w);
+  }
+  cnt += acc;
+  if constexpr (PV) {
+    uint32_t all = __popc(S[xw] & row[xw] & ~ax);
+    for (uint32_t w = 0; w < xw; w++) all += __popc(S[w] & row[w]);
+    all += acc;
+    if (all) atomicAdd(&c.pvl[x], ull(all));
+  }
+}
+
+// R == 2: sum over members x of |S ∩ N+(x)|, one member per lane.  Members
+// are scattered word by word (lane j takes bit j of the current non-empty
+// word) into the warp's 64-entry candidate queue, and a full batch of 32
+// runs its dot products; no lane ever pops bits serially.
 template <bool PV>
 __device__ ull dot_count(const WarpCtx& c, const uint32_t* S, uint32_t s) {
   (void)s;
   ull cnt = 0;
+  uint32_t qn = 0;
+  const uint32_t lane = c.lane, lt = (1u << lane) - 1u;
   for (uint32_t w0 = 0; w0 < c.W; w0 += 32) {
-    const uint32_t wl = w0 + c.lane;
-    uint32_t v = wl < c.W ? S[wl] : 0u;
-    while (__any_sync(FULL, v != 0)) {
-      const uint32_t n = __popc(v);
-      uint32_t incl = n;
-      for (int sh = 1; sh < 32; sh <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, sh);
-        if (c.lane >= uint32_t(sh)) incl += t;
+    const uint32_t wl = w0 + lane;
+    const uint32_t mine = wl < c.W ? S[wl] : 0u;
+    uint32_t nz = __ballot_sync(FULL, mine != 0);
+    while (nz) {
+      const uint32_t j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t v = __shfl_sync(FULL, mine, j);
+      if ((v >> lane) & 1u) c.cand[qn + __popc(v & lt)] = 32 * (w0 + j) + lane;
+      qn += __popc(v);
+      if (qn >= 32) {
+        __syncwarp();
+        const uint32_t x = c.cand[lane];
+        const bool mv = lane + 32 < qn;
+        const uint32_t x1 = mv ? c.cand[lane + 32] : 0u;
+        __syncwarp();
+        if (mv) c.cand[lane] = x1;
+        qn -= 32;
+        dot_member<PV>(c, S, x, cnt);
       }
-      const uint32_t tot = __shfl_sync(FULL, incl, 31);
-      for (uint32_t pos = incl - n; v && pos < 32; pos++, v &= v - 1)
-        c.cand[pos] = 32 * wl + __ffs(v) - 1;
-      __syncwarp();
-      if (c.lane < min(tot, 32u)) {
-        const uint32_t x = c.cand[c.lane];
-        const uint32_t* row = c.sym + size_t(x) * c.wp;
-        const uint32_t xw = x >> 5;
-        uint32_t acc = __popc(S[xw] & row[xw] & above_mask(x & 31));
-        for (uint32_t w = xw + 1; w < c.W; w++) acc += __popc(S[w] & row[w]);
-        cnt += acc;
-        if constexpr (PV) {
-          uint32_t all = __popc(S[xw] & row[xw] & ~above_mask(x & 31));
-          for (uint32_t w = 0; w < xw; w++) all += __popc(S[w] & row[w]);
-          all += acc;
-          if (all) atomicAdd(&c.pvl[x], ull(all));
-        }
-      }
-      __syncwarp();
     }
   }
+  __syncwarp();
+  if (lane < qn) dot_member<PV>(c, S, c.cand[lane], cnt);
+  __syncwarp();
   return warp_sum(cnt);
 }
 
@@ -549,8 +577,11 @@ struct CtaArgs {
 // GWS = false: the whole working set is dynamic shared memory (the
 // compiler sees shared-memory pointers and emits LDS/STS/ATOMS); true:
 // per-CTA slices of a global arena (heavy tier).
-template <bool PV, bool GWS, int NT, int MAXL>
-__global__ void __launch_bounds__(NT) count_cta_kernel(CtaArgs a) {
+// MB: minimum resident CTAs per SM the register allocation must allow (4
+// caps 256-thread CTAs at 64 registers for the staging-bound k = 4 pass; 3
+// gives the k >= 5 edge searches 80 registers without spills).
+template <bool PV, bool GWS, int NT, int MAXL, int MB>
+__global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_src, s_edge;
@@ -817,10 +848,10 @@ __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t
     pv[v] = pv_rank[rank[v]];
 }
 
-template <bool PV, bool GWS, int NT, int MAXL>
+template <bool PV, bool GWS, int NT, int MAXL, int MB = 1>
 void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget, cudaStream_t st) {
   const Device& dev = device();
-  auto kern = count_cta_kernel<PV, GWS, NT, MAXL>;
+  auto kern = count_cta_kernel<PV, GWS, NT, MAXL, MB>;
   unsigned grid;
   size_t smem = 0;
   if (!GWS) {
@@ -849,8 +880,12 @@ void launch_cta(Graph& g, CtaArgs a, bool global_ws, int nt, size_t heavy_budget
     launch_cta_t<PV, true, 512, MAXL>(g, a, heavy_budget, st);
   else if (nt == 512)
     launch_cta_t<PV, false, 512, MAXL>(g, a, heavy_budget, st);
-  else
-    launch_cta_t<PV, false, 256, MAXL>(g, a, heavy_budget, st);
+  else {
+    if constexpr (MAXL == 0) {
+      if (a.k == 4) return launch_cta_t<PV, false, 256, MAXL, 4>(g, a, heavy_budget, st);
+    }
+    launch_cta_t<PV, false, 256, MAXL, 3>(g, a, heavy_budget, st);
+  }
 }
 
 template <bool PV, int MAXL>
