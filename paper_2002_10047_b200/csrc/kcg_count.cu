@@ -473,6 +473,94 @@ __device__ ull dot_count(const WarpCtx& c, const uint32_t* S, uint32_t s) {
   return warp_sum(cnt);
 }
 
+// R == 3 (k = 5), totals: for an edge set S (|S| > 32) the number of
+// triangles of S's induced DAG, sum over members x and over y in
+// T_x = S ∩ N+(x) above x of |S ∩ N+(x) ∩ N+(y)| above y.  The warp walks x
+// in order, scatters T_x word by word into a 64-entry (x, y) queue (lane j
+// takes bit j) and every full batch runs 32 three-way dot products; T_x is
+// never stored and no DFS state is kept.
+__device__ ull pair_dots(const WarpCtx& c, const uint32_t* S) {
+  ull cnt = 0;
+  uint32_t qn = 0;
+  const uint32_t lane = c.lane, lt = (1u << lane) - 1u, W = c.W, G = (W + 3) >> 2;
+  uint32_t* qy = c.qy;       // 64 entries
+  uint32_t* qx = c.qy + 64;  // 64 entries
+  const uint4* S4 = reinterpret_cast<const uint4*>(S);
+  auto dot3 = [&](uint32_t x, uint32_t y) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(c.sym + size_t(x) * c.wp);
+    const uint4* y4 = reinterpret_cast<const uint4*>(c.sym + size_t(y) * c.wp);
+    const uint32_t yw = y >> 5, g0 = yw >> 2, b0 = g0 * 4, ay = above_mask(y & 31);
+    uint4 va = S4[g0], vb = x4[g0], vc = y4[g0];
+    uint32_t acc =
+        __popc(va.x & vb.x & vc.x & (b0 < yw ? 0u : (b0 == yw ? ay : FULL))) +
+        __popc(va.y & vb.y & vc.y & (b0 + 1 < yw ? 0u : (b0 + 1 == yw ? ay : FULL))) +
+        __popc(va.z & vb.z & vc.z & (b0 + 2 < yw ? 0u : (b0 + 2 == yw ? ay : FULL))) +
+        __popc(va.w & vb.w & vc.w & (b0 + 3 < yw ? 0u : (b0 + 3 == yw ? ay : FULL)));
+    for (uint32_t g = g0 + 1; g < G; g++) {
+      va = S4[g];
+      vb = x4[g];
+      vc = y4[g];
+      acc += __popc(va.x & vb.x & vc.x) + __popc(va.y & vb.y & vc.y) +
+             __popc(va.z & vb.z & vc.z) + __popc(va.w & vb.w & vc.w);
+    }
+    cnt += acc;
+  };
+  for (uint32_t s0 = 0; s0 < W; s0 += 32) {
+    const uint32_t sw = s0 + lane;
+    const uint32_t smine = sw < W ? S[sw] : 0u;
+    uint32_t snz = __ballot_sync(FULL, smine != 0);
+    while (snz) {
+      const uint32_t sj = __ffs(snz) - 1;
+      snz &= snz - 1;
+      uint32_t xb = __shfl_sync(FULL, smine, sj);
+      const uint32_t xw = s0 + sj;
+      while (xb) {
+        const uint32_t x = 32 * xw + __ffs(xb) - 1;
+        xb &= xb - 1;
+        const uint32_t* rx = c.sym + size_t(x) * c.wp;
+        for (uint32_t t0 = xw & ~31u; t0 < W; t0 += 32) {
+          const uint32_t tw = t0 + lane;
+          uint32_t t = 0;
+          if (tw < W && tw >= xw) t = S[tw] & rx[tw] & (tw == xw ? above_mask(x & 31) : FULL);
+          uint32_t tnz = __ballot_sync(FULL, t != 0);
+          while (tnz) {
+            const uint32_t tj = __ffs(tnz) - 1;
+            tnz &= tnz - 1;
+            const uint32_t v = __shfl_sync(FULL, t, tj);
+            if ((v >> lane) & 1u) {
+              const uint32_t pos = qn + __popc(v & lt);
+              qy[pos] = 32 * (t0 + tj) + lane;
+              qx[pos] = x;
+            }
+            qn += __popc(v);
+            if (qn >= 32) {
+              __syncwarp();
+              const uint32_t y0 = qy[lane], x0 = qx[lane];
+              const bool mv = lane + 32 < qn;
+              uint32_t y1 = 0, x1 = 0;
+              if (mv) {
+                y1 = qy[lane + 32];
+                x1 = qx[lane + 32];
+              }
+              __syncwarp();
+              if (mv) {
+                qy[lane] = y1;
+                qx[lane] = x1;
+              }
+              qn -= 32;
+              dot3(x0, y0);
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < qn) dot3(qx[lane], qy[lane]);
+  __syncwarp();
+  return warp_sum(cnt);
+}
+
 // child = S ∩ N+(x) into dst; returns |child| (warp-uniform)
 __device__ uint32_t child_set(const WarpCtx& c, const uint32_t* S, uint32_t x, uint32_t* dst) {
   const uint32_t* row = c.sym + size_t(x) * c.wp;
@@ -499,6 +587,7 @@ __device__ ull warp_count(const WarpCtx& c, uint32_t s, int R) {
   if (R == 1) return set_members_pv<PV>(c, S0);
   if (R == 2) return dot_count<PV>(c, S0, s);
   if (s <= 32) return compact_count<PV, MAXL>(c, S0, s, R);
+  if (!PV && R == 3) return pair_dots(c, S0);
   // warp-cooperative DFS over sets larger than 32
   Lvl* st = c.lvl;
   int L = 0;
@@ -541,6 +630,8 @@ __device__ ull warp_count(const WarpCtx& c, uint32_t s, int R) {
         add = dot_count<PV>(c, child, sc);
       } else if (sc <= 32) {
         add = compact_count<PV, MAXL>(c, child, sc, int(rc));
+      } else if (!PV && rc == 3) {
+        add = pair_dots(c, child);
       } else {
         descend = true;
       }
