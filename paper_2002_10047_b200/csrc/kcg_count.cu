@@ -988,11 +988,13 @@ inline size_t stacks_size(bool pv, int maxl) {
   return maxl > 8 ? stk_bytes<false, 32>() : stk_bytes<false, 8>();
 }
 
-// Edge slices per source: for k >= 5 the counting work of a large source
-// (roughly d * s^(k-2)) dwarfs its staging, so its edges are split over
-// several CTAs (each re-stages the bitmap); for k <= 4 staging dominates.
+// Edge slices per source: only deep searches (k >= 8) pay for splitting a
+// large source's edges over several CTAs, each re-staging its bitmap; up to
+// k = 7 the per-edge warp scheduling inside one CTA balances well enough
+// that re-staging costs more than it saves (config 2 k=5: 164 ms with
+// d/64 slices vs 133 ms without; config 3 k=8: 463 vs 512 ms).
 inline uint32_t slices_for(uint32_t d, int k) {
-  if (k < 5 || d <= 128) return 1;
+  if (k < 8 || d <= 128) return 1;
   return std::min<uint32_t>(64, d / 64);
 }
 
