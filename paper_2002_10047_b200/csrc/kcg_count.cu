@@ -197,12 +197,12 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
           }
           if (__ldg(adj + rb + lo) == target) {
             atomicOr(&sym[r], 1u << j);
-            atomicOr(&sym[j], 1u << r);
+            if constexpr (PV) atomicOr(&sym[j], 1u << r);
           }
         }
       }
       my_staged += T;
-      Stager st{M, sym, 1, S.qy, S.qi, lane, 0};
+      Stager<PV> st{M, sym, 1, S.qy, S.qi, lane, 0};
       const Rows rl{S.P, S.rbase, S.rowid, nl};
       stage_long(rl, st, adj, 0, Ll);
       const Rows rs{S.P + nl + 1, S.rbase + nl, S.rowid + nl, ns};
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     // stage the induced subgraph: each warp one contiguous 1/NW of the
     // long-row elements and of the short-row elements
     {
-      Stager st{M, sym, wp, c.qy, c.qy + 64, lane, 0};
+      Stager<PV> st{M, sym, wp, c.qy, c.qy + 64, lane, 0};
       const Rows rl{rP, rbase, rowid, nl};
       stage_long(rl, st, a.adj, uint32_t(uint64_t(Ll) * wib / NW),
                  uint32_t(uint64_t(Ll) * (wib + 1) / NW));
@@ -805,23 +805,28 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
         const uint32_t* ri = sym + size_t(i) * wp;
         uint32_t bits = ri[w];
         if (w == (i >> 5)) bits &= above_mask(i & 31);
+        if (!bits) continue;
+        // row i's words after w in w's 16-byte group, masked once; word w
+        // itself is `bits`, which after popping x is exactly row_i[w] above x
+        const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
+        const uint32_t g0 = w >> 2, G = (W + 3) >> 2, wj = w & 3;
+        uint4 vp = ri4[g0];
+        vp.x = 0;
+        if (wj >= 1) vp.y = 0;
+        if (wj >= 2) vp.z = 0;
+        if (wj >= 3) vp.w = 0;
         ull ci = 0;
         while (bits) {
           const uint32_t x = 32 * w + __ffs(bits) - 1;
           bits &= bits - 1;
           const uint32_t* rx = sym + size_t(x) * wp;
           // |row_i ∩ row_x| above x, 4 words per 128-bit load
-          const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
           const uint4* rx4 = reinterpret_cast<const uint4*>(rx);
-          const uint32_t g0 = w >> 2, G = (W + 3) >> 2, ax = above_mask(x & 31);
-          uint4 va = ri4[g0], vb = rx4[g0];
-          const uint32_t b0 = g0 * 4;
-          uint32_t cx = __popc(va.x & vb.x & (b0 < w ? 0u : (b0 == w ? ax : FULL))) +
-                        __popc(va.y & vb.y & (b0 + 1 < w ? 0u : (b0 + 1 == w ? ax : FULL))) +
-                        __popc(va.z & vb.z & (b0 + 2 < w ? 0u : (b0 + 2 == w ? ax : FULL))) +
-                        __popc(va.w & vb.w & (b0 + 3 < w ? 0u : (b0 + 3 == w ? ax : FULL)));
+          uint4 vb = rx4[g0];
+          uint32_t cx = __popc(bits & rx[w]) + __popc(vp.y & vb.y) + __popc(vp.z & vb.z) +
+                        __popc(vp.w & vb.w);
           for (uint32_t g = g0 + 1; g < G; g++) {
-            va = ri4[g];
+            const uint4 va = ri4[g];
             vb = rx4[g];
             cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
                   __popc(va.w & vb.w);

@@ -67,7 +67,10 @@ struct Rows {
   uint32_t nr;
 };
 
-// Warp-private batching of filter-passing candidates.
+// Warp-private batching of filter-passing candidates.  SYM: also set the
+// mirrored bit (row j, column i); only the per-vertex paths read the lower
+// triangle, every counting path reads rows above their own index.
+template <bool SYM>
 struct Stager {
   Member M;
   uint32_t* sym;
@@ -81,7 +84,7 @@ struct Stager {
     const uint32_t j = member_probe(M, y);
     if (j != NOTFOUND) {
       atomicOr(&sym[i * wp + (j >> 5)], 1u << (j & 31));
-      atomicOr(&sym[j * wp + (i >> 5)], 1u << (i & 31));
+      if constexpr (SYM) atomicOr(&sym[j * wp + (i >> 5)], 1u << (i & 31));
     }
   }
   __device__ __forceinline__ void push(bool pass, uint32_t y, uint32_t row) {
@@ -132,7 +135,8 @@ __device__ __forceinline__ uint32_t row_search(const Rows& R, uint32_t pbeg) {
 }
 
 // Short rows: virtual positions [pbeg, pend), 32 per chunk.
-__device__ __forceinline__ void stage_short(const Rows& R, Stager& S,
+template <class ST>
+__device__ __forceinline__ void stage_short(const Rows& R, ST& S,
                                             const uint32_t* __restrict__ adj, uint32_t pbeg,
                                             uint32_t pend) {
   if (pbeg >= pend) return;
@@ -171,7 +175,8 @@ __device__ __forceinline__ void stage_short(const Rows& R, Stager& S,
 }
 
 // Long rows (>= 32 entries): a lane's row is one compare per chunk.
-__device__ __forceinline__ void stage_long(const Rows& R, Stager& S,
+template <class ST>
+__device__ __forceinline__ void stage_long(const Rows& R, ST& S,
                                            const uint32_t* __restrict__ adj, uint32_t pbeg,
                                            uint32_t pend) {
   if (pbeg >= pend) return;
