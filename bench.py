@@ -18,7 +18,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -74,56 +73,62 @@ def config_obj(cfg_id, spec, k, g, extra=None):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clocks and clock-event reasons every ~5 ms through NVML on
+    a background thread while the timed region runs (nvidia-smi's -lms loop
+    needs ~0.3 s to start, longer than a short timed region)."""
 
-    def __init__(self, index=0):
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self, index=0, period_s=0.005):
         self.index = index
+        self.period = period_s
         self.rows = []
-        self.proc = None
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() \
+                else self.index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - no NVML: report unsampled
+            self.nv = None
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(self.period)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-        rows = self.rows
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
-        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4)
-                          if r[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        self._stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS
+                          if rs & getattr(self.nv, attr, 0)})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.rows),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML, every %.0f ms during the timed steps" % (1e3 * self.period)}
 
 
 def measured_peaks():
@@ -338,19 +343,26 @@ def run_kcg(args):
         adj_p = torch.from_numpy(g.adj.view(np.int32)).pin_memory()
         e_steps = max(1, min(args.steps, 5))
         e_times = []
+        split = np.zeros(3)
         for i in range(max(args.warmup, 3) + e_steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             he = kcg.DeviceGraph.from_csr_ptr(g.n, off_p.data_ptr(), adj_p.data_ptr())
+            t1 = time.perf_counter()
             te, _ = he.pipeline(strat, eps, k)
+            t2 = time.perf_counter()
             he.close()
+            t3 = time.perf_counter()
             if i >= max(args.warmup, 3):
-                e_times.append(time.perf_counter() - t0)
+                e_times.append(t3 - t0)
+                split += (t1 - t0, t2 - t1, t3 - t2)
             assert te == total
         esec = sum(e_times) / len(e_times)
+        split *= 1e3 / len(e_times)
         e2e = {"value": total / esec, "unit": "cliques/s",
                "h2d_bytes_per_step": int(off_p.numel() * 8 + adj_p.numel() * 4),
                "d2h_bytes_per_step": 8, "ms_per_step": esec * 1e3,
+               "split_ms": {"create_h2d": split[0], "pipeline": split[1], "destroy": split[2]},
                "path": "kcg_graph_create(pinned host CSR) + kcg_pipeline + destroy"}
 
     cpu = None
