@@ -9,8 +9,9 @@
  *
  * Conventions
  *  - Every call returns a status: KCG_OK, KCG_EINVAL (the cases where the
- *    reference throws std::invalid_argument), KCG_ERUNTIME (CUDA/runtime
- *    failure), KCG_ENOMEM (device or host allocation failed).
+ *    reference throws std::invalid_argument), KCG_ELOGIC (where it throws
+ *    std::logic_error), KCG_ERUNTIME (CUDA/runtime failure), KCG_ENOMEM
+ *    (device or host allocation failed).
  *    kcg_last_error() returns the calling thread's last message.
  *  - Host buffers are caller-allocated; device memory is owned by the
  *    kcg_graph handle and stays resident across calls.
@@ -35,6 +36,7 @@ extern "C" {
 #define KCG_EINVAL 1
 #define KCG_ERUNTIME 2
 #define KCG_ENOMEM 3
+#define KCG_ELOGIC 4  /* the reference's std::logic_error cases (peeling) */
 
 /* OrientStrategy (proj/include/kclique/orientation.hpp:10-16), same order. */
 #define KCG_DEGREE 0
@@ -135,6 +137,40 @@ int kcg_per_vertex_device(kcg_graph* g, const uint64_t** d_per_vertex);
  * (the benchmark's step).  per_vertex may be NULL. */
 int kcg_pipeline(kcg_graph* g, int strategy, double eps, uint64_t alpha_hat,
                  int k, uint64_t* total, uint64_t* per_vertex);
+
+/* ---- Peeling: consumers of the per-vertex counts (SURVEY.md §8(f) row 1,
+ * proj/include/kclique/peeling.hpp:59-92).  The handle must hold the
+ * undirected graph (kcg_graph_create) and a ranking (kcg_rank or
+ * kcg_set_ranking); the DAG is built on demand.  Cliques are counted on the
+ * device by restricted recounts (kcg_peel.cu). */
+
+/* PeelOutcome (peeling.hpp:67-76) minus its arrays. */
+typedef struct kcg_peel_result {
+  uint64_t rounds;         /* extraction rounds */
+  uint64_t total_cliques;  /* k-clique count of the input graph */
+  double best_density;     /* max over rounds of remaining cliques / remaining vertices */
+  uint64_t best_round;     /* first round attaining it (0 = before any removal) */
+  uint64_t num_dense;      /* entries written to dense_vertices */
+} kcg_peel_result;
+
+/* update_counts (peeling.hpp:58-63, peeling.cpp:114-200): removes the
+ * batch (batch_len distinct ids) from the graph minus the `peeled` flags
+ * (n bytes), subtracts from counts (n u64, host, in/out) the k-cliques each
+ * survivor loses, and reports the destroyed cliques and the survivors
+ * whose count dropped (ascending ids; `changed` holds n entries).
+ * KCG_EINVAL for k < 2 or a batch vertex that is out of range or peeled;
+ * KCG_ELOGIC when a count would go negative (counts inconsistent). */
+int kcg_update_counts(kcg_graph* g, int k, uint64_t* counts, const uint32_t* batch,
+                      uint64_t batch_len, const uint8_t* peeled, uint64_t* removed,
+                      uint32_t* changed, uint64_t* changed_len);
+/* peel_exact (peeling.hpp:80, peeling.cpp:202-245).  core (n u64) and
+ * dense_vertices (n u32) are optional host outputs. */
+int kcg_peel_exact(kcg_graph* g, int k, kcg_peel_result* out, uint64_t* core,
+                   uint32_t* dense_vertices);
+/* peel_approx (peeling.hpp:87-92, peeling.cpp:247-320); KCG_EINVAL for
+ * k < 2 or eps <= 0. */
+int kcg_peel_approx(kcg_graph* g, int k, double eps, kcg_peel_result* out,
+                    uint32_t* dense_vertices);
 
 int kcg_timings(const kcg_graph* g, kcg_times* out);
 int kcg_last_count_stats(const kcg_graph* g, kcg_count_stats* out);

@@ -362,3 +362,156 @@ int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
   free(c.bufs), free(c.chain), free(c.stamp);
   return 0;
 }
+
+/* ---- peeling --------------------------------- */
+
+/* Per-vertex k-clique counts of the subgraph induced by the live vertices
+ * (dead ones isolated), by recounting from scratch: the residual graph is
+ * degree-ordered and counted with kco_count.  This is the "sequential
+ * recounting reference" the reference's own peeling tests compare against
+ * (proj/tests/test_peeling.cpp:23-52, testutil.hpp reference_peel). */
+static int kco_residual(uint32_t n, const uint64_t* off, const uint32_t* adj,
+                        const uint8_t* live, int k, uint64_t* total, uint64_t* pv) {
+  uint64_t* roff = calloc((size_t)n + 1, sizeof(uint64_t));
+  uint64_t two_m = off[n];
+  uint32_t* radj = malloc((two_m ? two_m : 1) * sizeof(uint32_t));
+  uint32_t* rank = malloc(((size_t)n + 1) * sizeof(uint32_t));
+  uint64_t* doff = malloc(((size_t)n + 1) * sizeof(uint64_t));
+  uint32_t* dadj = malloc((two_m ? two_m : 1) * sizeof(uint32_t));
+  int rc = 3;
+  if (!roff || !radj || !rank || !doff || !dadj) goto out;
+  for (uint32_t v = 0; v < n; v++) {
+    roff[v + 1] = roff[v];
+    if (!live[v]) continue;
+    for (uint64_t p = off[v]; p < off[v + 1]; p++)
+      if (live[adj[p]]) radj[roff[v + 1]++] = adj[p];
+  }
+  if ((rc = kco_rank_degree(n, roff, rank))) goto out;
+  if ((rc = kco_direct(n, roff, radj, rank, doff, dadj))) goto out;
+  rc = kco_count(n, doff, dadj, k, total, pv);
+out:
+  free(roff);
+  free(radj);
+  free(rank);
+  free(doff);
+  free(dadj);
+  return rc;
+}
+
+/* update_counts, src/peeling.cpp:114-200, restated as recount differencing
+ * (test_peeling.cpp:101-148 checks the reference against exactly this):
+ * every survivor u loses pv_A[u] - pv_{A\B}[u] cliques, removed =
+ * tot_A - tot_{A\B}.  Status 1 for a peeled / out-of-range batch vertex
+ * (peeling.cpp:133-136), 4 when a count would go negative (159-161).
+ * changed (n capacity) receives the survivors whose count dropped,
+ * ascending. */
+int kco_update_counts(uint32_t n, const uint64_t* off, const uint32_t* adj, int k,
+                      uint64_t* counts, const uint32_t* batch, uint64_t nb,
+                      const uint8_t* peeled, uint64_t* removed, uint32_t* changed,
+                      uint64_t* nchanged) {
+  if (k < 2) return 1;
+  for (uint64_t i = 0; i < nb; i++)
+    if (batch[i] >= n || peeled[batch[i]]) return 1;
+  uint8_t* live = malloc((size_t)n + 1);
+  uint64_t* pa = malloc(((size_t)n + 1) * sizeof(uint64_t));
+  uint64_t* pb = malloc(((size_t)n + 1) * sizeof(uint64_t));
+  int rc = 3;
+  if (!live || !pa || !pb) goto out;
+  for (uint32_t v = 0; v < n; v++) live[v] = !peeled[v];
+  uint64_t ta = 0, tb = 0;
+  if ((rc = kco_residual(n, off, adj, live, k, &ta, pa))) goto out;
+  for (uint64_t i = 0; i < nb; i++) live[batch[i]] = 0;
+  if ((rc = kco_residual(n, off, adj, live, k, &tb, pb))) goto out;
+  int under = 0;
+  *nchanged = 0;
+  for (uint32_t v = 0; v < n; v++) {
+    if (!live[v]) continue;
+    uint64_t d = pa[v] - pb[v];
+    if (d > counts[v]) under = 1;
+    counts[v] -= d;
+    if (d) changed[(*nchanged)++] = v;
+  }
+  *removed = ta - tb;
+  rc = under ? 4 : 0;
+out:
+  free(live);
+  free(pa);
+  free(pb);
+  return rc;
+}
+
+/* peel_exact / peel_approx, src/peeling.cpp:202-320: rounds extract every
+ * live vertex of minimum count (exact; core = running max of the extracted
+ * values) or every live vertex with double(count) <= k (1+eps) rem / alive
+ * (approx), counts recomputed from scratch on the residual graph each
+ * round; best density compared as exact fractions (peeling.cpp:196-211).
+ * res = {rounds, total, best_round, num_dense}; core (n, exact only) and
+ * dense (n) are outputs. */
+int kco_peel(uint32_t n, const uint64_t* off, const uint32_t* adj, int k, int exact,
+             double eps, uint64_t* res, double* density, uint64_t* core, uint32_t* dense) {
+  if (k < 2) return 1;
+  if (!exact && !(eps > 0)) return 1;
+  memset(res, 0, 4 * sizeof(uint64_t));
+  *density = 0.0;
+  if (n == 0) return 0;
+  uint8_t* live = malloc(n);
+  uint64_t* cur = malloc((size_t)n * sizeof(uint64_t));
+  uint64_t* round_of = malloc((size_t)n * sizeof(uint64_t));
+  int rc = 3;
+  if (!live || !cur || !round_of) goto out;
+  memset(live, 1, n);
+  uint64_t total = 0;
+  if ((rc = kco_residual(n, off, adj, live, k, &total, cur))) goto out;
+  res[1] = total;
+  uint64_t best_c = 0, best_a = 1, best_r = 0;
+  if ((unsigned __int128)total * best_a > (unsigned __int128)best_c * n) {
+    best_c = total;
+    best_a = n;
+  }
+  uint64_t rem = total, alive = n, round = 0, level = 0;
+  while (alive > 0) {
+    round++;
+    uint64_t mn = UINT64_MAX;
+    double cutoff = 0;
+    if (exact) {
+      for (uint32_t v = 0; v < n; v++)
+        if (live[v] && cur[v] < mn) mn = cur[v];
+      if (mn > level) level = mn;
+    } else {
+      cutoff = (double)k * (1.0 + eps) * ((double)rem / (double)alive);
+    }
+    uint64_t nb = 0;
+    for (uint32_t v = 0; v < n; v++) {
+      if (!live[v]) continue;
+      if (exact ? cur[v] == mn : (double)cur[v] <= cutoff) {
+        live[v] = 0;
+        round_of[v] = round;
+        if (exact) core[v] = level;
+        nb++;
+      }
+    }
+    if (nb == 0) {
+      rc = 4;
+      goto out;
+    }
+    alive -= nb;
+    if ((rc = kco_residual(n, off, adj, live, k, &rem, cur))) goto out;
+    if (alive && (unsigned __int128)rem * best_a > (unsigned __int128)best_c * alive) {
+      best_c = rem;
+      best_a = alive;
+      best_r = round;
+    }
+  }
+  res[0] = round;
+  res[2] = best_r;
+  res[3] = 0;
+  for (uint32_t v = 0; v < n; v++)
+    if (round_of[v] > best_r) dense[res[3]++] = v;
+  *density = best_a ? (double)best_c / (double)best_a : 0.0;
+  rc = 0;
+out:
+  free(live);
+  free(cur);
+  free(round_of);
+  return rc;
+}

@@ -7,13 +7,14 @@
 //
 // Every entry point maps the reference's exceptions onto the same status
 // codes as the product C ABI (include/kcg.h): 0 ok, 1 invalid argument,
-// 2 runtime error, 3 out of memory.
+// 2 runtime error, 3 out of memory, 4 logic error.
 #include <omp.h>
 
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <new>
+#include <span>
 #include <stdexcept>
 #include <vector>
 
@@ -21,6 +22,7 @@
 #include "kclique/graph.hpp"
 #include "kclique/oracle.hpp"
 #include "kclique/orientation.hpp"
+#include "kclique/peeling.hpp"
 
 using namespace kclique;
 
@@ -33,6 +35,8 @@ int guarded(F&& f) {
     return 0;
   } catch (const std::invalid_argument&) {
     return 1;
+  } catch (const std::logic_error&) {
+    return 4;
   } catch (const std::bad_alloc&) {
     return 3;
   } catch (...) {
@@ -187,6 +191,45 @@ int ref_brute_force(void* g, int k, uint64_t* total, uint64_t* pv) {
 
 int ref_exact_arboricity(void* g, uint64_t* out) {
   return guarded([&] { *out = oracle::exact_arboricity(*static_cast<Graph*>(g)); });
+}
+
+// update_counts (peeling.cpp:194-200): counts in/out (n), changed out (n
+// capacity).
+int ref_update_counts(void* g, void* dg, int k, uint64_t* counts, const uint32_t* batch,
+                      uint64_t batch_len, const uint8_t* peeled, uint64_t* removed,
+                      uint32_t* changed, uint64_t* changed_len) {
+  return guarded([&] {
+    const Graph& G = *static_cast<Graph*>(g);
+    const uint32_t n = G.num_vertices();
+    UpdateResult r = update_counts(G, *static_cast<DirectedGraph*>(dg), k,
+                                   std::span<uint64_t>(counts, n),
+                                   std::span<const VertexId>(batch, batch_len),
+                                   std::span<const uint8_t>(peeled, n));
+    *removed = r.removed;
+    *changed_len = r.changed.size();
+    if (!r.changed.empty()) std::memcpy(changed, r.changed.data(), r.changed.size() * 4);
+  });
+}
+
+// peel_exact / peel_approx (peeling.cpp:202-320).  res = {rounds, total,
+// best_round, num_dense}; core (n, exact only) and dense (n) may be null.
+int ref_peel(void* g, void* dg, int k, int exact, double eps, uint64_t* res, double* density,
+             uint64_t* core, uint32_t* dense, double* seconds) {
+  return guarded([&] {
+    const Graph& G = *static_cast<Graph*>(g);
+    const double t0 = now_s();
+    PeelOutcome o = exact ? peel_exact(G, *static_cast<DirectedGraph*>(dg), k)
+                          : peel_approx(G, *static_cast<DirectedGraph*>(dg), k, eps);
+    if (seconds) *seconds = now_s() - t0;
+    res[0] = o.rounds;
+    res[1] = o.total_cliques;
+    res[2] = o.best_round;
+    res[3] = o.dense_vertices.size();
+    *density = o.best_density;
+    if (core && !o.core.empty()) std::memcpy(core, o.core.data(), o.core.size() * 8);
+    if (dense && !o.dense_vertices.empty())
+      std::memcpy(dense, o.dense_vertices.data(), o.dense_vertices.size() * 4);
+  });
 }
 
 }  // extern "C"

@@ -113,6 +113,9 @@ void Graph::release_all() {
   scratch3.release();
   heavy.release();
   counters.release();
+  live_off.release();
+  live_adj.release();
+  peel_ws.release();
 }
 
 Graph::~Graph() {
@@ -482,6 +485,51 @@ int kcg_pipeline(kcg_graph* h, int strategy, double eps, uint64_t alpha_hat, int
       g.times.download_ms = g.elapsed(4, 5);
     }
     if (total) *total = t;
+  });
+}
+
+int kcg_update_counts(kcg_graph* h, int k, uint64_t* counts, const uint32_t* batch,
+                      uint64_t batch_len, const uint8_t* peeled, uint64_t* removed,
+                      uint32_t* changed, uint64_t* changed_len) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    g.times.d2h_bytes = 0;
+    UpdateOut r = update_counts(g, k, counts, batch, batch_len, peeled);
+    if (removed) *removed = r.removed;
+    if (changed && !r.changed.empty())
+      std::memcpy(changed, r.changed.data(), r.changed.size() * 4);
+    if (changed_len) *changed_len = r.changed.size();
+  });
+}
+
+namespace {
+void peel_result(const PeelOut& r, kcg_peel_result* out, uint32_t* dense) {
+  if (out) {
+    out->rounds = r.rounds;
+    out->total_cliques = r.total;
+    out->best_density = r.best_density;
+    out->best_round = r.best_round;
+    out->num_dense = r.dense.size();
+  }
+  if (dense && !r.dense.empty()) std::memcpy(dense, r.dense.data(), r.dense.size() * 4);
+}
+}  // namespace
+
+int kcg_peel_exact(kcg_graph* h, int k, kcg_peel_result* out, uint64_t* core,
+                   uint32_t* dense_vertices) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    g.times.d2h_bytes = 0;
+    peel_result(peel(g, k, true, 0.0, core), out, dense_vertices);
+  });
+}
+
+int kcg_peel_approx(kcg_graph* h, int k, double eps, kcg_peel_result* out,
+                    uint32_t* dense_vertices) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    g.times.d2h_bytes = 0;
+    peel_result(peel(g, k, false, eps, nullptr), out, dense_vertices);
   });
 }
 

@@ -899,15 +899,18 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
 // ---------------------------------------------------------------------------
 // Splits sources with d >= dmin into the warp tier list and the CTA/heavy
 // candidate list (key = d for sorting).
+// smask (rank space, optional): only sources r with smask[r] != 0 (the
+// peeling updates count the region around a batch, kcg_peel.cu).
 __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, uint32_t dmin,
                                 uint32_t part, uint32_t nparts,
+                                const uint8_t* __restrict__ smask,
                                 uint32_t* __restrict__ wlist, uint32_t* __restrict__ clist,
                                 uint32_t* __restrict__ ckey, unsigned* __restrict__ cnt) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const uint32_t r = base + threadIdx.x;
     uint32_t d = 0;
-    if (r < n && r % nparts == part) d = uint32_t(off[r + 1] - off[r]);
+    if (r < n && r % nparts == part && (!smask || smask[r])) d = uint32_t(off[r + 1] - off[r]);
     const bool inw = r < n && d >= dmin && d <= 32;
     const bool inc = r < n && d >= dmin && d > 32;
     unsigned bw = __ballot_sync(FULL, inw), bc = __ballot_sync(FULL, inc);
@@ -927,15 +930,25 @@ __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, ui
   }
 }
 
-__global__ void k2_pv_kernel(const uint64_t* __restrict__ rdag_off,
-                             const uint32_t* __restrict__ rdag_adj, uint32_t n, uint32_t part,
-                             uint32_t nparts, ull* __restrict__ pv_rank) {
+// k = 2 (counting.cpp:165-173): every directed edge of a selected source is
+// a 2-clique; the total is summed on the device so that partial and
+// source-masked counts need no host pass over the offsets.
+__global__ void k2_kernel(const uint64_t* __restrict__ rdag_off,
+                          const uint32_t* __restrict__ rdag_adj, uint32_t n, uint32_t part,
+                          uint32_t nparts, const uint8_t* __restrict__ smask,
+                          ull* __restrict__ pv_rank, ull* __restrict__ total) {
+  ull t = 0;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (r % nparts != part) continue;
+    if (r % nparts != part || (smask && !smask[r])) continue;
     const uint64_t b = rdag_off[r], e = rdag_off[r + 1];
-    if (e > b) atomicAdd(&pv_rank[r], ull(e - b));
-    for (uint64_t p = b; p < e; p++) atomicAdd(&pv_rank[rdag_adj[p]], 1ull);
+    t += e - b;
+    if (pv_rank) {
+      if (e > b) atomicAdd(&pv_rank[r], ull(e - b));
+      for (uint64_t p = b; p < e; p++) atomicAdd(&pv_rank[rdag_adj[p]], 1ull);
+    }
   }
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(total, t);
 }
 
 __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t* __restrict__ rank,
@@ -1022,23 +1035,14 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     g.pv.ensure(size_t(n) + 1, &g.alloc);
     KCG_CUDA(cudaMemsetAsync(g.pv_rank.p, 0, size_t(n) * 8, g.stream));
   }
-  uint64_t total = 0;
   if (k == 2) {
-    // counting.cpp:165-173: every directed edge is a 2-clique
-    total = nparts == 1 ? g.m : 0;
-    if (nparts > 1) {
-      std::vector<uint64_t> ro(size_t(n) + 1);
-      KCG_CUDA(cudaMemcpyAsync(ro.data(), g.rdag_off.p, ro.size() * 8, cudaMemcpyDeviceToHost,
-                               g.stream));
-      g.sync();
-      for (uint32_t r = part; r < n; r += nparts) total += ro[r + 1] - ro[r];
-    }
-    if (want_pv && n) {
-      k2_pv_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, n,
-                                                            part, nparts, PVR(g));
+    g.mark(6);
+    if (n) {
+      k2_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, n, part,
+                                                         nparts, g.src_mask,
+                                                         want_pv ? PVR(g) : nullptr, ctr);
       KCG_LAUNCHED(g);
     }
-    g.mark(6);
     g.mark(7);
   } else if (uint64_t(k - 1) <= g.max_out) {
     // tier lists
@@ -1052,7 +1056,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     uint32_t* ckey2 = reinterpret_cast<uint32_t*>(sb + 4 * nb);
     unsigned* cnt = reinterpret_cast<unsigned*>(ctr + 2);
     classify_kernel<<<blocks_for(n, 256, 148u * 16u), 256, 0, g.stream>>>(
-        g.rdag_off.p, n, dmin, part, nparts, wlist, clist, ckey, cnt);
+        g.rdag_off.p, n, dmin, part, nparts, g.src_mask, wlist, clist, ckey, cnt);
     KCG_LAUNCHED(g);
     unsigned hc[2] = {0, 0};
     KCG_CUDA(cudaMemcpyAsync(hc, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
@@ -1232,7 +1236,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
   KCG_CUDA(cudaMemcpyAsync(hv, ctr, 16, cudaMemcpyDeviceToHost, g.stream));
   g.mark(3);
   g.sync();
-  if (k != 2) total = hv[0];
+  const uint64_t total = hv[0];
   g.stats.staged_elems = hv[1];
   g.times.count_ms = g.elapsed(2, 3);
   g.times.count_kernel_ms = g.elapsed(6, 7);

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "kcg.h"
 
@@ -143,6 +144,14 @@ struct Graph {
   DevBuf<unsigned char> heavy;     // heavy-tier global bitmaps
   DevBuf<unsigned long long> counters;  // small device counters
   PinnedBuf pinned;
+  // peeling (kcg_peel.cu): the DAG restricted to the live vertices, swapped
+  // in for rdag_* while counting, and the per-round state
+  DevBuf<uint64_t> live_off;
+  DevBuf<uint32_t> live_adj;
+  DevBuf<unsigned char> peel_ws;
+  // counting restricted to sources r with src_mask[r] != 0 (rank space);
+  // nullptr = every source
+  const uint8_t* src_mask = nullptr;
 
   kcg_times times{};
   kcg_count_stats stats{};
@@ -171,6 +180,20 @@ void build_dag(Graph& g, bool want_id_dag);
 void relabel_from_dag(Graph& g);  // rdag from an adopted id-space DAG
 uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part = 0,
                        uint32_t nparts = 1);
+
+// peeling consumers of the per-vertex counts (kcg_peel.cu)
+struct UpdateOut {
+  uint64_t removed = 0;
+  std::vector<uint32_t> changed;
+};
+UpdateOut update_counts(Graph& g, int k, uint64_t* counts, const uint32_t* batch,
+                        uint64_t batch_len, const uint8_t* peeled);
+struct PeelOut {
+  uint64_t rounds = 0, total = 0, best_round = 0;
+  double best_density = 0.0;
+  std::vector<uint32_t> dense;
+};
+PeelOut peel(Graph& g, int k, bool exact, double eps, uint64_t* core_out);
 
 // small helpers
 void* cub_temp(Graph& g, size_t bytes);

@@ -20,7 +20,7 @@ import numpy as np
 
 from ._paths import LIB_DIR
 
-KCG_OK, KCG_EINVAL, KCG_ERUNTIME, KCG_ENOMEM = 0, 1, 2, 3
+KCG_OK, KCG_EINVAL, KCG_ERUNTIME, KCG_ENOMEM, KCG_ELOGIC = 0, 1, 2, 3, 4
 DEGREE, ORIGINAL, KCORE, GOODRICH_PSZONA, BARENBOIM_ELKIN = 0, 1, 2, 3, 4
 STRATEGY_NAMES = {"degree": DEGREE, "original": ORIGINAL, "kcore": KCORE,
                   "goodrich_pszona": GOODRICH_PSZONA, "barenboim_elkin": BARENBOIM_ELKIN}
@@ -31,7 +31,7 @@ EXPORTED = [
     "kcg_num_edges", "kcg_rank", "kcg_estimate_arboricity", "kcg_set_ranking", "kcg_direct",
     "kcg_count", "kcg_per_vertex_device", "kcg_pipeline", "kcg_timings",
     "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
-    "kcg_stream",
+    "kcg_stream", "kcg_update_counts", "kcg_peel_exact", "kcg_peel_approx",
 ]
 
 
@@ -43,6 +43,16 @@ class KcgError(RuntimeError):
 
 class KcgOutOfMemory(KcgError, MemoryError):
     pass
+
+
+class KcgLogicError(KcgError):
+    """The reference's std::logic_error cases (peeling)."""
+
+
+class PeelResult(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_uint64), ("total_cliques", ctypes.c_uint64),
+                ("best_density", ctypes.c_double), ("best_round", ctypes.c_uint64),
+                ("num_dense", ctypes.c_uint64)]
 
 
 class Times(ctypes.Structure):
@@ -110,6 +120,9 @@ def lib():
         L.kcg_device_bytes.argtypes = [vp]
         L.kcg_device_bytes.restype = u64
         L.kcg_synchronize.argtypes = [vp]
+        L.kcg_update_counts.argtypes = [vp, ctypes.c_int, vp, vp, u64, vp, P(u64), vp, P(u64)]
+        L.kcg_peel_exact.argtypes = [vp, ctypes.c_int, P(PeelResult), vp, vp]
+        L.kcg_peel_approx.argtypes = [vp, ctypes.c_int, ctypes.c_double, P(PeelResult), vp]
         _lib = L
     return _lib
 
@@ -122,6 +135,8 @@ def _check(rc: int):
         raise ValueError(msg)  # std::invalid_argument in the reference
     if rc == KCG_ENOMEM:
         raise KcgOutOfMemory(rc, msg)
+    if rc == KCG_ELOGIC:
+        raise KcgLogicError(rc, msg)
     raise KcgError(rc, msg)
 
 
@@ -275,6 +290,46 @@ class DeviceGraph:
 
     def synchronize(self):
         _check(lib().kcg_synchronize(self._h))
+
+    # ---- peeling (kcg_peel.cu; peeling.hpp:58-92) ----
+    def update_counts(self, k, counts, batch, peeled):
+        """update_counts: returns (removed, changed ids); `counts` (u64
+        numpy array, n entries) is updated in place."""
+        n = self.n
+        if counts.dtype != np.uint64 or not counts.flags.c_contiguous or len(counts) < n:
+            raise TypeError("counts must be a contiguous uint64 array of n entries")
+        b = _u32(batch)
+        pe = np.ascontiguousarray(peeled, dtype=np.uint8)
+        removed = ctypes.c_uint64(0)
+        nch = ctypes.c_uint64(0)
+        changed = np.zeros(max(n, 1), np.uint32)
+        _check(lib().kcg_update_counts(self._h, int(k), counts.ctypes.data, b.ctypes.data,
+                                       len(b), pe.ctypes.data, ctypes.byref(removed),
+                                       changed.ctypes.data, ctypes.byref(nch)))
+        return int(removed.value), changed[:nch.value].copy()
+
+    def peel_exact(self, k):
+        """peel_exact: dict(rounds, total_cliques, best_density, best_round,
+        core, dense_vertices)."""
+        n = self.n
+        r = PeelResult()
+        core = np.zeros(max(n, 1), np.uint64)
+        dense = np.zeros(max(n, 1), np.uint32)
+        _check(lib().kcg_peel_exact(self._h, int(k), ctypes.byref(r), core.ctypes.data,
+                                    dense.ctypes.data))
+        return {"rounds": r.rounds, "total_cliques": r.total_cliques,
+                "best_density": r.best_density, "best_round": r.best_round,
+                "core": core[:n].copy(), "dense_vertices": dense[:r.num_dense].copy()}
+
+    def peel_approx(self, k, eps):
+        n = self.n
+        r = PeelResult()
+        dense = np.zeros(max(n, 1), np.uint32)
+        _check(lib().kcg_peel_approx(self._h, int(k), float(eps), ctypes.byref(r),
+                                     dense.ctypes.data))
+        return {"rounds": r.rounds, "total_cliques": r.total_cliques,
+                "best_density": r.best_density, "best_round": r.best_round,
+                "dense_vertices": dense[:r.num_dense].copy()}
 
 
 # ---- reference-shaped entry points ------------------------------------------

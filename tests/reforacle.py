@@ -29,9 +29,15 @@ class OracleError(Exception):
     pass
 
 
+class OracleLogicError(OracleError):
+    pass
+
+
 def _check(rc, what):
     if rc == 1:
         raise ValueError(f"{what}: invalid argument")
+    if rc == 4:
+        raise OracleLogicError(f"{what}: logic error")
     if rc != 0:
         raise OracleError(f"{what}: status {rc}")
 
@@ -65,6 +71,10 @@ class Ref:
         L.ref_brute_force.argtypes = [vp, ctypes.c_int, P(ctypes.c_uint64), vp]
         L.ref_exact_arboricity.argtypes = [vp, P(ctypes.c_uint64)]
         L.ref_set_threads.argtypes = [ctypes.c_int]
+        L.ref_update_counts.argtypes = [vp, vp, ctypes.c_int, vp, vp, ctypes.c_uint64, vp,
+                                        P(ctypes.c_uint64), vp, P(ctypes.c_uint64)]
+        L.ref_peel.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, vp,
+                               P(ctypes.c_double), vp, vp, P(ctypes.c_double)]
         self.L = L
 
     def set_threads(self, t):
@@ -155,6 +165,35 @@ class Ref:
         _check(self.L.ref_brute_force(h, k, ctypes.byref(total), pv.ctypes.data), "brute")
         return int(total.value), pv[:n]
 
+    def update_counts(self, h, dg, n, k, counts, batch, peeled):
+        """Reference update_counts; counts (u64, n) updated in place."""
+        b = _arr(batch, np.uint32)
+        pe = _arr(peeled, np.uint8)
+        removed = ctypes.c_uint64(0)
+        nch = ctypes.c_uint64(0)
+        changed = np.zeros(max(n, 1), np.uint32)
+        _check(self.L.ref_update_counts(h, dg, k, counts.ctypes.data, b.ctypes.data, len(b),
+                                        pe.ctypes.data, ctypes.byref(removed),
+                                        changed.ctypes.data, ctypes.byref(nch)),
+               "update_counts")
+        return int(removed.value), changed[:nch.value].copy()
+
+    def peel(self, h, dg, n, k, exact, eps=0.5):
+        res = np.zeros(4, np.uint64)
+        dens = ctypes.c_double(0)
+        secs = ctypes.c_double(0)
+        core = np.zeros(max(n, 1), np.uint64)
+        dense = np.zeros(max(n, 1), np.uint32)
+        _check(self.L.ref_peel(h, dg, k, int(exact), float(eps), res.ctypes.data,
+                               ctypes.byref(dens), core.ctypes.data, dense.ctypes.data,
+                               ctypes.byref(secs)), "peel")
+        out = {"rounds": int(res[0]), "total_cliques": int(res[1]),
+               "best_round": int(res[2]), "best_density": float(dens.value),
+               "dense_vertices": dense[:int(res[3])].copy(), "seconds": float(secs.value)}
+        if exact:
+            out["core"] = core[:n].copy()
+        return out
+
     def exact_arboricity(self, h):
         out = ctypes.c_uint64(0)
         _check(self.L.ref_exact_arboricity(h, ctypes.byref(out)), "arboricity")
@@ -180,6 +219,11 @@ class Port:
         L.kco_count.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, P(ctypes.c_uint64), vp]
         L.kco_alg_bytes.argtypes = [ctypes.c_uint32, vp, vp]
         L.kco_alg_bytes.restype = ctypes.c_uint64
+        L.kco_update_counts.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, vp, vp,
+                                        ctypes.c_uint64, vp, P(ctypes.c_uint64), vp,
+                                        P(ctypes.c_uint64)]
+        L.kco_peel.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_double, vp, P(ctypes.c_double), vp, vp]
         self.L = L
 
     def rank_degree(self, g):
@@ -226,3 +270,33 @@ class Port:
     def alg_bytes(self, n, off, adj):
         off, adj = _arr(off, np.uint64), _arr(adj, np.uint32)
         return int(self.L.kco_alg_bytes(n, off.ctypes.data, adj.ctypes.data))
+
+    def update_counts(self, g, k, counts, batch, peeled):
+        """Recount-differencing restatement of update_counts; counts (u64,
+        n) updated in place.  Returns (removed, changed)."""
+        b = _arr(batch, np.uint32)
+        pe = _arr(peeled, np.uint8)
+        removed = ctypes.c_uint64(0)
+        nch = ctypes.c_uint64(0)
+        changed = np.zeros(max(g.n, 1), np.uint32)
+        _check(self.L.kco_update_counts(g.n, g.offsets.ctypes.data, g.adj.ctypes.data, k,
+                                        counts.ctypes.data, b.ctypes.data, len(b),
+                                        pe.ctypes.data, ctypes.byref(removed),
+                                        changed.ctypes.data, ctypes.byref(nch)),
+               "update_counts")
+        return int(removed.value), changed[:nch.value].copy()
+
+    def peel(self, g, k, exact, eps=0.5):
+        res = np.zeros(4, np.uint64)
+        dens = ctypes.c_double(0)
+        core = np.zeros(max(g.n, 1), np.uint64)
+        dense = np.zeros(max(g.n, 1), np.uint32)
+        _check(self.L.kco_peel(g.n, g.offsets.ctypes.data, g.adj.ctypes.data, k, int(exact),
+                               float(eps), res.ctypes.data, ctypes.byref(dens),
+                               core.ctypes.data, dense.ctypes.data), "peel")
+        out = {"rounds": int(res[0]), "total_cliques": int(res[1]),
+               "best_round": int(res[2]), "best_density": float(dens.value),
+               "dense_vertices": dense[:int(res[3])].copy()}
+        if exact:
+            out["core"] = core[:g.n].copy()
+        return out

@@ -1,0 +1,121 @@
+"""GPU parity of the peeling consumers (kcg_update_counts, kcg_peel_exact,
+kcg_peel_approx; kcg_peel.cu) against the reference's outputs in
+tests/golden/peel_cases.json and the reference's known answers
+(proj/tests/test_peeling.cpp).  Every call goes through the C ABI."""
+import numpy as np
+import pytest
+
+from paper_2002_10047_b200 import gen, kcg
+from tests import peelcases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return peelcases.load()
+
+
+def complete(n):
+    return gen.from_edges(n, np.array([(i, j) for i in range(n) for j in range(i + 1, n)]))
+
+
+def oriented(g, strat=kcg.DEGREE, eps=1.0):
+    h = kcg.DeviceGraph.from_graph(g)
+    h.rank(strat, eps, download=False)
+    return h
+
+
+def test_update_sequences(cases):
+    for case in cases["updates"]:
+        g = peelcases.graph(case["graph"])
+        k = case["k"]
+        with oriented(g) as h:
+            counts = np.array(case["initial"], np.uint64)
+            h.direct(download=False)
+            _, pv = h.count(k, per_vertex=True)
+            assert pv.tolist() == case["initial"]
+            peeled = np.zeros(g.n, np.uint8)
+            for st in case["steps"]:
+                removed, changed = h.update_counts(k, counts, st["batch"], peeled)
+                peeled[st["batch"]] = 1
+                assert removed == st["removed"], (case["graph"]["params"], k)
+                assert changed.tolist() == st["changed"]
+                assert counts.tolist() == st["counts"]
+
+
+def test_peel_outcomes(cases):
+    for case in cases["peels"]:
+        g = peelcases.graph(case["graph"])
+        with oriented(g, case["strategy"], case["strategy_eps"]) as h:
+            out = h.peel_exact(case["k"]) if case["exact"] else \
+                h.peel_approx(case["k"], case["eps"])
+        peelcases.check_outcome(case, out, "gpu")
+
+
+def test_known_answers_and_errors():
+    g = complete(4)
+    with oriented(g) as h:
+        counts = np.full(4, 3, np.uint64)
+        removed, changed = h.update_counts(3, counts, [0], np.zeros(4, np.uint8))
+        assert removed == 3 and changed.tolist() == [1, 2, 3]
+        assert counts.tolist() == [3, 1, 1, 1]
+        counts = np.full(4, 3, np.uint64)
+        removed, changed = h.update_counts(3, counts, [0, 1, 2, 3], np.zeros(4, np.uint8))
+        assert removed == 4 and changed.tolist() == []
+        pe = np.zeros(4, np.uint8)
+        pe[2] = 1
+        with pytest.raises(ValueError):
+            h.update_counts(3, np.full(4, 3, np.uint64), [1, 2], pe)
+        with pytest.raises(ValueError):
+            h.update_counts(3, np.full(4, 3, np.uint64), [7], np.zeros(4, np.uint8))
+        with pytest.raises(ValueError):
+            h.update_counts(1, np.full(4, 3, np.uint64), [0], np.zeros(4, np.uint8))
+        # inconsistent counts: a decrement below zero is the reference's
+        # std::logic_error (peeling.cpp:174-175)
+        with pytest.raises(kcg.KcgLogicError):
+            h.update_counts(3, np.zeros(4, np.uint64), [0], np.zeros(4, np.uint8))
+        with pytest.raises(ValueError):
+            h.peel_exact(1)
+        with pytest.raises(ValueError):
+            h.peel_approx(3, 0.0)
+        with pytest.raises(ValueError):
+            h.peel_approx(3, -1.0)
+    with oriented(complete(5)) as h:
+        out = h.peel_exact(3)
+        assert out["total_cliques"] == 10 and out["rounds"] == 1
+        assert out["best_density"] == 2.0 and out["best_round"] == 0
+        assert out["core"].tolist() == [6] * 5
+        assert out["dense_vertices"].tolist() == [0, 1, 2, 3, 4]
+    with oriented(gen.from_edges(0, np.zeros((0, 2), np.int64))) as h:
+        out = h.peel_exact(3)
+        assert out["rounds"] == 0 and out["total_cliques"] == 0
+
+
+def test_peel_approx_config2_properties():
+    """Full-size R-MAT s20: approximate peeling of the 4-clique counts.
+    Size-independent checks: the clique total equals kcg_count's, the best
+    density is at least the whole graph's, rounds are O(log n) and the
+    dense set's own 4-clique density (recounted on the induced subgraph)
+    equals the reported best density."""
+    g = gen.load_config_graph(2, cache=False)
+    spec = gen.CONFIGS[2]
+    with oriented(g, spec["strategy"], spec["eps"]) as h:
+        h.direct(download=False)
+        total, _ = h.count(4)
+        out = h.peel_approx(4, 0.5)
+    assert out["total_cliques"] == total
+    assert out["best_density"] >= total / g.n
+    assert out["rounds"] <= 4 * 21 + 2
+    dense = out["dense_vertices"]
+    keep = np.zeros(g.n, bool)
+    keep[dense] = True
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets).astype(np.int64))
+    sel = keep[src] & keep[g.adj] & (src < g.adj)
+    local = np.full(g.n, -1, np.int64)
+    local[dense] = np.arange(len(dense))
+    sub = gen.from_edges(len(dense), np.stack([local[src[sel]], local[g.adj[sel]]], 1))
+    with oriented(sub) as hs:
+        hs.direct(download=False)
+        t_sub, _ = hs.count(4)
+    assert t_sub / len(dense) == out["best_density"]
