@@ -1,7 +1,8 @@
 // RAII wrapper over the kcg C ABI, shared by the drop-in translation units.
 // Status codes map back onto the reference's exception types
 // (SURVEY.md §8(b)): KCG_EINVAL -> std::invalid_argument,
-// KCG_ENOMEM -> std::bad_alloc, anything else -> std::runtime_error.
+// KCG_ENOMEM -> std::bad_alloc, KCG_ELOGIC -> std::logic_error, anything
+// else -> std::runtime_error.
 #pragma once
 
 #include <new>
@@ -18,6 +19,7 @@ inline void check(int rc) {
   std::string msg = kcg_last_error();
   if (rc == KCG_EINVAL) throw std::invalid_argument(msg);
   if (rc == KCG_ENOMEM) throw std::bad_alloc();
+  if (rc == KCG_ELOGIC) throw std::logic_error(msg);
   throw std::runtime_error("kcg: " + msg);
 }
 

@@ -1,7 +1,8 @@
 // Drop-in check: compiled against the repo's include/kclique/*.hpp and
 // linked against libkclique_b200.so (which runs on the B200), exercising
 // the reference API the way the reference's own unit tests do
-// (proj/tests/test_counting.cpp, test_orientation.cpp, test_graph.cpp).
+// (proj/tests/test_counting.cpp, test_orientation.cpp, test_graph.cpp,
+// test_peeling.cpp, test_bucket_queue.cpp).
 // The expected values are the reference's known answers; the brute-force
 // checker below is an independent exhaustive enumeration.
 //
@@ -20,6 +21,7 @@
 #include "kclique/counting.hpp"
 #include "kclique/graph.hpp"
 #include "kclique/orientation.hpp"
+#include "kclique/peeling.hpp"
 
 using namespace kclique;
 
@@ -324,6 +326,158 @@ void case_default_parallelism() {
   CHECK(default_parallelism(8) == Parallelism::edge);
 }
 
+// ---- peeling (proj/tests/test_peeling.cpp, test_bucket_queue.cpp) ----
+
+void case_bucket_queue() {
+  std::vector<uint64_t> vals = {5, 3, 9, 3, 5, 0};
+  BucketQueue q(vals);
+  CHECK(q.size() == 6);
+  auto [v0, b0] = q.extract_min();
+  CHECK(v0 == 0 && b0 == std::vector<VertexId>{5});
+  auto [v1, b1] = q.extract_min();
+  CHECK(v1 == 3 && (b1 == std::vector<VertexId>{1, 3}));
+  auto [v2, b2] = q.extract_min();
+  CHECK(v2 == 5 && (b2 == std::vector<VertexId>{0, 4}));
+  auto [v3, b3] = q.extract_min();
+  CHECK(v3 == 9 && b3 == std::vector<VertexId>{2});
+  CHECK(q.empty());
+  CHECK_THROWS_AS(q.extract_min(), std::logic_error);
+  std::vector<uint64_t> v2s = {10, 20, 30};
+  BucketQueue r(v2s);
+  r.update(2, 1);
+  CHECK(r.extract_min().first == 1);
+  r.update(0, 500);
+  CHECK(r.extract_min().first == 20);
+  r.update(0, 499);
+  r.update(0, 7);
+  auto [w, bw] = r.extract_min();
+  CHECK(w == 7 && bw == std::vector<VertexId>{0});
+  CHECK_THROWS_AS(r.update(0, 3), std::logic_error);
+  std::vector<uint64_t> v3s = {8, 8, 8};
+  BucketQueue s3(v3s);
+  s3.update(1, 3);
+  CHECK(s3.value(1) == 3);
+}
+
+void case_update_counts() {
+  Graph g = complete(4);
+  DirectedGraph dg = oriented(g);
+  std::vector<uint64_t> counts(4, 3);
+  std::vector<uint8_t> peeled(4, 0);
+  std::vector<VertexId> batch = {0};
+  UpdateResult res = update_counts(g, dg, 3, counts, batch, peeled);
+  CHECK(res.removed == 3);
+  CHECK((res.changed == std::vector<VertexId>{1, 2, 3}));
+  CHECK(counts[1] == 1 && counts[2] == 1 && counts[3] == 1);
+  std::vector<uint64_t> c2(4, 3);
+  std::vector<VertexId> all = {0, 1, 2, 3};
+  res = update_counts(g, dg, 3, c2, all, peeled);
+  CHECK(res.removed == 4 && res.changed.empty());
+  peeled[2] = 1;
+  std::vector<VertexId> b2 = {1, 2};
+  CHECK_THROWS_AS(update_counts(g, dg, 3, c2, b2, peeled), std::invalid_argument);
+  std::vector<uint8_t> none(4, 0);
+  std::vector<uint64_t> zeros(4, 0);
+  CHECK_THROWS_AS(update_counts(g, dg, 3, zeros, batch, none), std::logic_error);
+  // recount differencing on random residual graphs (test_peeling.cpp:101-148)
+  std::mt19937_64 rng(5);
+  for (uint64_t seed = 0; seed < 6; seed++) {
+    Graph h = gnp(12, 0.45, seed + 2200);
+    DirectedGraph dh = oriented(h);
+    for (int k : {3, 4}) {
+      std::vector<uint8_t> pe(12, 0);
+      std::vector<uint64_t> cur = brute(h, k).pv;
+      std::vector<VertexId> alive(12);
+      std::iota(alive.begin(), alive.end(), 0);
+      while (!alive.empty()) {
+        std::shuffle(alive.begin(), alive.end(), rng);
+        size_t take = 1 + rng() % std::min<size_t>(alive.size(), 4);
+        std::vector<VertexId> bt(alive.begin(), alive.begin() + take);
+        std::sort(bt.begin(), bt.end());
+        // residual before/after by exhaustive count
+        auto residual = [&](const std::vector<uint8_t>& dead) {
+          std::vector<std::pair<VertexId, VertexId>> e;
+          for (VertexId v = 0; v < 12; v++)
+            for (VertexId u : h.neighbors(v))
+              if (v < u && !dead[v] && !dead[u]) e.emplace_back(v, u);
+          return brute(Graph::from_edges(12, std::move(e)), k);
+        };
+        Brute before = residual(pe);
+        UpdateResult ur = update_counts(h, dh, k, cur, bt, pe);
+        for (VertexId v : bt) pe[v] = 1;
+        alive.erase(alive.begin(), alive.begin() + take);
+        Brute after = residual(pe);
+        CHECK(ur.removed == before.total - after.total);
+        std::vector<VertexId> ch;
+        for (VertexId v = 0; v < 12; v++) {
+          if (pe[v]) continue;
+          CHECK(cur[v] == after.pv[v]);
+          if (after.pv[v] != before.pv[v]) ch.push_back(v);
+        }
+        CHECK(ur.changed == ch);
+      }
+    }
+  }
+}
+
+void case_peel() {
+  Graph k5 = complete(5);
+  PeelOutcome out = peel_exact(k5, oriented(k5), 3);
+  CHECK(out.total_cliques == 10 && out.rounds == 1 && out.best_density == 2.0);
+  CHECK(out.best_round == 0 && out.core == std::vector<uint64_t>(5, 6));
+  CHECK((out.dense_vertices == std::vector<VertexId>{0, 1, 2, 3, 4}));
+  Graph two = Graph::from_edges(6, {{0, 1}, {1, 2}, {0, 2}, {3, 4}, {4, 5}, {3, 5}});
+  out = peel_exact(two, oriented(two), 3);
+  CHECK(out.total_cliques == 2 && out.rounds == 1 && out.best_density == 2.0 / 6.0);
+  CHECK(out.core == std::vector<uint64_t>(6, 1) && out.dense_vertices.size() == 6);
+  out = peel_approx(k5, oriented(k5), 3, 0.5);
+  CHECK(out.rounds == 1 && out.best_density == 2.0 && out.dense_vertices.size() == 5);
+  Graph p = path_graph(8);
+  out = peel_approx(p, oriented(p), 3, 0.5);
+  CHECK(out.total_cliques == 0 && out.rounds == 1 && out.best_density == 0.0);
+  CHECK_THROWS_AS(peel_exact(k5, oriented(k5), 1), std::invalid_argument);
+  CHECK_THROWS_AS(peel_approx(k5, oriented(k5), 3, 0.0), std::invalid_argument);
+  // exact peeling == sequential recounting (test_peeling.cpp:173-192)
+  for (uint64_t seed = 0; seed < 10; seed++) {
+    Graph g = gnp(VertexId(8 + seed % 7), 0.5, seed + 5100);
+    const VertexId n = g.num_vertices();
+    for (int k : {3, 4}) {
+      PeelOutcome ex = peel_exact(g, oriented(g), k);
+      std::vector<uint8_t> dead(n, 0);
+      std::vector<uint64_t> core(n, 0), when(n, 0);
+      uint64_t level = 0, rounds = 0, alive = n, bc = 0, ba = 1, br = 0;
+      Brute b = brute(g, k);
+      if (b.total * ba > bc * n) bc = b.total, ba = n;
+      while (alive) {
+        rounds++;
+        uint64_t mn = UINT64_MAX;
+        for (VertexId v = 0; v < n; v++)
+          if (!dead[v]) mn = std::min(mn, b.pv[v]);
+        level = std::max(level, mn);
+        std::vector<VertexId> bt;
+        for (VertexId v = 0; v < n; v++)
+          if (!dead[v] && b.pv[v] == mn) bt.push_back(v);
+        for (VertexId v : bt) dead[v] = 1, core[v] = level, when[v] = rounds;
+        alive -= bt.size();
+        std::vector<std::pair<VertexId, VertexId>> e;
+        for (VertexId v = 0; v < n; v++)
+          for (VertexId u : g.neighbors(v))
+            if (v < u && !dead[v] && !dead[u]) e.emplace_back(v, u);
+        b = brute(Graph::from_edges(n, std::move(e)), k);
+        if (alive && b.total * ba > bc * alive) bc = b.total, ba = alive, br = rounds;
+      }
+      std::vector<VertexId> dense;
+      for (VertexId v = 0; v < n; v++)
+        if (when[v] > br) dense.push_back(v);
+      CHECK(ex.core == core);
+      CHECK(ex.rounds == rounds);
+      CHECK(ex.best_round == br);
+      CHECK(ex.best_density == double(bc) / double(ba));
+      CHECK(ex.dense_vertices == dense);
+    }
+  }
+}
+
 }  // namespace
 
 int main() {
@@ -344,6 +498,9 @@ int main() {
       {"directed graph properties", case_dag_properties},
       {"graph construction and text io", case_graph_io},
       {"default parallelism", case_default_parallelism},
+      {"bucket queue", case_bucket_queue},
+      {"update_counts", case_update_counts},
+      {"peel_exact / peel_approx", case_peel},
   };
   for (auto& c : cases) {
     int before = g_fail;
