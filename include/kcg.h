@@ -94,6 +94,21 @@ int kcg_graph_create_device(uint32_t n, uint64_t m, const uint64_t* d_offsets,
 int kcg_dag_create(uint32_t n, const uint64_t* out_offsets,
                    const uint32_t* out_targets, const uint32_t* rank,
                    kcg_graph** out);
+/* Graph::from_edges (graph.cpp:11-41) on the device: `count` edges
+ * (host arrays us[i], vs[i]) are swapped to u < v, self-loops dropped,
+ * sorted, deduplicated and symmetrised into the CSR the handle keeps.
+ * KCG_EINVAL if an endpoint is >= n (the reference's invalid_argument). */
+int kcg_graph_from_edges(uint32_t n, const uint32_t* us, const uint32_t* vs,
+                         uint64_t count, kcg_graph** out);
+/* The benchmark's R-MAT generator on the device (2^scale vertices,
+ * `samples` draws, quadrant probabilities a, b, c, 1-a-b-c, optional seeded
+ * id permutation), normalised like kcg_graph_from_edges.  Bit-identical to
+ * the host generator (csrc/gen/kcgen.cpp kcgen_rmat). */
+int kcg_graph_rmat(int scale, uint64_t samples, double a, double b, double c,
+                   uint64_t seed, int permute, kcg_graph** out);
+/* Downloads the handle's undirected CSR (offsets n+1, adjacency 2m);
+ * either pointer may be NULL. */
+int kcg_graph_csr(kcg_graph* g, uint64_t* offsets, uint32_t* adj);
 void kcg_graph_destroy(kcg_graph* g);
 uint32_t kcg_num_vertices(const kcg_graph* g);
 uint64_t kcg_num_edges(const kcg_graph* g);

@@ -337,6 +337,51 @@ int kcg_dag_create(uint32_t n, const uint64_t* out_offsets, const uint32_t* out_
   });
 }
 
+int kcg_graph_from_edges(uint32_t n, const uint32_t* us, const uint32_t* vs, uint64_t count,
+                         kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    if (count && (!us || !vs)) fail(KCG_EINVAL, "edge arrays are null");
+    auto* g = new Graph();
+    try {
+      g->times = kcg_times{};
+      build_from_edges(*g, n, us, vs, count);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(g);
+  });
+}
+
+int kcg_graph_rmat(int scale, uint64_t samples, double a, double b, double c, uint64_t seed,
+                   int permute, kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    auto* g = new Graph();
+    try {
+      g->times = kcg_times{};
+      build_rmat(*g, scale, samples, a, b, c, seed, permute != 0);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(g);
+  });
+}
+
+int kcg_graph_csr(kcg_graph* h, uint64_t* offsets, uint32_t* adj) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!g.has_und) fail(KCG_EINVAL, "handle holds no undirected graph");
+    if (offsets) download(g, offsets, g.und_off.p, (size_t(g.n) + 1) * 8);
+    if (adj) download(g, adj, g.und_adj.p, 2 * g.m * 4);
+    g.sync();
+  });
+}
+
 void kcg_graph_destroy(kcg_graph* h) {
   try {
     delete reinterpret_cast<Graph*>(h);

@@ -181,6 +181,12 @@ void relabel_from_dag(Graph& g);  // rdag from an adopted id-space DAG
 uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part = 0,
                        uint32_t nparts = 1);
 
+// input construction on the device (kcg_build.cu)
+void build_from_edges(Graph& g, uint32_t n, const uint32_t* us, const uint32_t* vs,
+                      uint64_t cnt);
+void build_rmat(Graph& g, int scale, uint64_t samples, double a, double b, double c,
+                uint64_t seed, bool permute);
+
 // peeling consumers of the per-vertex counts (kcg_peel.cu)
 struct UpdateOut {
   uint64_t removed = 0;

@@ -210,6 +210,7 @@ CONFIGS = {
             strategy=DEGREE, eps=1.0, ks=[3, 4], pv_ks=[3, 4],
             desc="Erdos-Renyi G(n=20000, m=200000), seed 1, degree order"),
     2: dict(name="rmat_s20_e16", build=lambda: rmat(20, 1 << 24, seed=2, permute=True),
+            rmat=dict(scale=20, samples=1 << 24, seed=2, permute=True),
             strategy=BARENBOIM_ELKIN, eps=0.5, ks=[4, 5], pv_ks=[],
             desc="R-MAT scale 20, 16,777,216 samples, (0.57,0.19,0.19,0.05), seed 2, "
                  "permuted; Barenboim-Elkin eps=0.5"),
@@ -222,6 +223,7 @@ CONFIGS = {
             strategy=KCORE, eps=1.0, ks=[6, 8], pv_ks=[6],
             desc="Random geometric graph n=2M, mean degree 48, seed 4; degeneracy order"),
     5: dict(name="rmat_s24_e32", build=lambda: rmat(24, 1 << 29, seed=5, permute=False),
+            rmat=dict(scale=24, samples=1 << 29, seed=5, permute=False),
             strategy=DEGREE, eps=1.0, ks=[4], pv_ks=[4],
             desc="R-MAT scale 24, edge factor 32 (536,870,912 samples), seed 5; "
                  "degree order; full pipeline"),

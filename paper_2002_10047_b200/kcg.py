@@ -32,6 +32,7 @@ EXPORTED = [
     "kcg_count", "kcg_per_vertex_device", "kcg_pipeline", "kcg_timings",
     "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
     "kcg_stream", "kcg_update_counts", "kcg_peel_exact", "kcg_peel_approx",
+    "kcg_graph_from_edges", "kcg_graph_rmat", "kcg_graph_csr",
 ]
 
 
@@ -120,6 +121,10 @@ def lib():
         L.kcg_device_bytes.argtypes = [vp]
         L.kcg_device_bytes.restype = u64
         L.kcg_synchronize.argtypes = [vp]
+        L.kcg_graph_from_edges.argtypes = [u32, vp, vp, u64, P(vp)]
+        L.kcg_graph_rmat.argtypes = [ctypes.c_int, u64, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, u64, ctypes.c_int, P(vp)]
+        L.kcg_graph_csr.argtypes = [vp, vp, vp]
         L.kcg_update_counts.argtypes = [vp, ctypes.c_int, vp, vp, u64, vp, P(u64), vp, P(u64)]
         L.kcg_peel_exact.argtypes = [vp, ctypes.c_int, P(PeelResult), vp, vp]
         L.kcg_peel_approx.argtypes = [vp, ctypes.c_int, ctypes.c_double, P(PeelResult), vp]
@@ -176,6 +181,33 @@ class DeviceGraph:
         _check(lib().kcg_graph_create(n, ctypes.c_void_p(offsets_ptr), ctypes.c_void_p(adj_ptr),
                                       ctypes.byref(h)))
         return cls(h)
+
+    @classmethod
+    def from_edges(cls, n: int, edges) -> "DeviceGraph":
+        """Graph::from_edges normalisation on the device (kcg_build.cu)."""
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        if len(e) and (e.min() < 0 or e.max() >= 1 << 32):
+            raise ValueError("edge endpoint out of range")
+        us, vs = _u32(e[:, 0]), _u32(e[:, 1])
+        h = ctypes.c_void_p()
+        _check(lib().kcg_graph_from_edges(int(n), us.ctypes.data, vs.ctypes.data, len(e),
+                                          ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def rmat(cls, scale, samples, a=0.57, b=0.19, c=0.19, seed=0, permute=False):
+        """The R-MAT generator on the device (same graph as gen.rmat)."""
+        h = ctypes.c_void_p()
+        _check(lib().kcg_graph_rmat(int(scale), int(samples), float(a), float(b), float(c),
+                                    int(seed), int(bool(permute)), ctypes.byref(h)))
+        return cls(h)
+
+    def csr(self):
+        """(offsets u64[n+1], adjacency u32[2m]) of the undirected graph."""
+        off = np.zeros(self.n + 1, np.uint64)
+        adj = np.zeros(max(2 * self.m, 1), np.uint32)
+        _check(lib().kcg_graph_csr(self._h, off.ctypes.data, adj.ctypes.data))
+        return off, adj[:2 * self.m]
 
     @classmethod
     def from_graph(cls, g) -> "DeviceGraph":
