@@ -256,6 +256,7 @@ struct Lvl {
 struct Layout {
   uint32_t dmax, wpmax, tbits, fbits, levels;
   size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
+  size_t sym_bytes;  // the bitmap; inside `total` unless sym_apart
   // per-warp offsets
   size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk, w_q;
   size_t total;
@@ -268,8 +269,10 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // different rows at the same offset spread over the banks.
 __host__ __device__ inline uint32_t row_stride(uint32_t W) { return 4u * (((W + 3u) >> 2) | 1u); }
 
+// sym_apart: the bitmap is laid out separately (a per-CTA slice of global
+// memory) and `total` covers the rest, which stays in shared memory.
 __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bool pv, int nw,
-                                              size_t stk_bytes) {
+                                              size_t stk_bytes, bool sym_apart = false) {
   Layout L;
   L.dmax = dmax;
   L.wpmax = row_stride((dmax + 31) / 32);
@@ -280,7 +283,8 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   L.levels = levels;
   size_t at = 0;
   L.sym = at;
-  at = align_up(at + size_t(dmax) * L.wpmax * 4, 16);
+  L.sym_bytes = align_up(size_t(dmax) * L.wpmax * 4, 128);
+  if (!sym_apart) at = align_up(at + size_t(dmax) * L.wpmax * 4, 16);
   L.table = at;
   at = align_up(at + (size_t(1) << tb) * 8, 16);
   L.filter = at;
@@ -671,7 +675,14 @@ struct CtaArgs {
 // MB: minimum resident CTAs per SM the register allocation must allow (4
 // caps 256-thread CTAs at 64 registers for the staging-bound k = 4 pass; 3
 // gives the k >= 5 edge searches 80 registers without spills).
-template <bool PV, bool GWS, int NT, int MAXL, int MB>
+// GWS (working set): WS_SMEM -- everything in dynamic shared memory;
+// WS_SYM_GLOBAL -- the bitmap in a per-CTA slice of global memory (L2),
+// hash table, filter, row lists and warp areas in shared memory;
+// WS_GLOBAL -- everything in the global slice (sources too large for the
+// shared part).
+constexpr int WS_SMEM = 0, WS_SYM_GLOBAL = 1, WS_GLOBAL = 2;
+
+template <bool PV, int GWS, int NT, int MAXL, int MB>
 __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -681,11 +692,17 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   __shared__ typename BlockScanU64::TempStorage s_scan;
   const Layout& L = a.L;
   unsigned char* base;
-  if constexpr (GWS)
+  uint32_t* sym;
+  if constexpr (GWS == WS_GLOBAL) {
     base = a.gbase + size_t(blockIdx.x) * L.total;
-  else
+    sym = reinterpret_cast<uint32_t*>(base + L.sym);
+  } else if constexpr (GWS == WS_SYM_GLOBAL) {
     base = smem;
-  uint32_t* sym = reinterpret_cast<uint32_t*>(base + L.sym);
+    sym = reinterpret_cast<uint32_t*>(a.gbase + size_t(blockIdx.x) * L.sym_bytes);
+  } else {
+    base = smem;
+    sym = reinterpret_cast<uint32_t*>(base + L.sym);
+  }
   ull* table = reinterpret_cast<ull*>(base + L.table);
   uint32_t* filter = reinterpret_cast<uint32_t*>(base + L.filter);
   uint32_t* rP = reinterpret_cast<uint32_t*>(base + L.rP);
@@ -957,19 +974,31 @@ __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t
     pv[v] = pv_rank[rank[v]];
 }
 
-template <bool PV, bool GWS, int NT, int MAXL, int MB = 1>
+// bytes of the global arena one CTA of this working-set mode needs
+inline size_t ws_global_bytes(int gws, const Layout& L) {
+  return gws == WS_GLOBAL ? L.total : gws == WS_SYM_GLOBAL ? L.sym_bytes : 0;
+}
+
+template <bool PV, int GWS, int NT, int MAXL, int MB = 1>
 void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget, cudaStream_t st) {
   const Device& dev = device();
   auto kern = count_cta_kernel<PV, GWS, NT, MAXL, MB>;
   unsigned grid;
   size_t smem = 0;
-  if (!GWS) {
+  if (GWS != WS_GLOBAL) {
     smem = a.L.total;
     KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = 0;
     KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
     grid = unsigned(std::min<uint64_t>(a.nitems, uint64_t(dev.sms) * std::max(occ, 1)));
-  } else {
+  }
+  if (GWS == WS_SYM_GLOBAL) {
+    // as many resident CTAs as the arena (sized by the caller) holds
+    const uint64_t fit = std::min<uint64_t>(heavy_budget, g.heavy.n) / a.L.sym_bytes;
+    if (fit == 0) fail(KCG_ERUNTIME, "heavy arena too small");
+    grid = unsigned(std::min<uint64_t>(grid, fit));
+    a.gbase = g.heavy.p;
+  } else if (GWS == WS_GLOBAL) {
     const size_t per = a.L.total;
     const uint64_t fit = std::max<uint64_t>(1, heavy_budget / per);
     grid = unsigned(std::min<uint64_t>({a.nitems, uint64_t(dev.sms) * 2, fit}));
@@ -982,18 +1011,19 @@ void launch_cta_t(Graph& g, CtaArgs a, size_t heavy_budget, cudaStream_t st) {
 }
 
 template <bool PV, int MAXL>
-void launch_cta(Graph& g, CtaArgs a, bool global_ws, int nt, size_t heavy_budget,
-                cudaStream_t st) {
+void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaStream_t st) {
   KCG_CUDA(cudaMemsetAsync(a.work, 0, 4, st));
-  if (global_ws)
-    launch_cta_t<PV, true, 512, MAXL>(g, a, heavy_budget, st);
+  if (gws == WS_GLOBAL)
+    launch_cta_t<PV, WS_GLOBAL, 512, MAXL>(g, a, heavy_budget, st);
+  else if (gws == WS_SYM_GLOBAL)
+    launch_cta_t<PV, WS_SYM_GLOBAL, 512, MAXL>(g, a, heavy_budget, st);
   else if (nt == 512)
-    launch_cta_t<PV, false, 512, MAXL>(g, a, heavy_budget, st);
+    launch_cta_t<PV, WS_SMEM, 512, MAXL>(g, a, heavy_budget, st);
   else {
     if constexpr (MAXL == 0) {
-      if (a.k == 4) return launch_cta_t<PV, false, 256, MAXL, 4>(g, a, heavy_budget, st);
+      if (a.k == 4) return launch_cta_t<PV, WS_SMEM, 256, MAXL, 4>(g, a, heavy_budget, st);
     }
-    launch_cta_t<PV, false, 256, MAXL, 3>(g, a, heavy_budget, st);
+    launch_cta_t<PV, WS_SMEM, 256, MAXL, 3>(g, a, heavy_budget, st);
   }
 }
 
@@ -1156,15 +1186,26 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       struct Plan {
         uint32_t lo, hi;
         Layout L;
-        bool gws;
+        int gws;  // WS_*
         int nt;
       };
       std::vector<Plan> plans;
-      // heavy: d > SMEM_TIER_MAX, working sets in global memory
+      const size_t smem_cap = size_t(dev.smem_optin) - 1024;
+      // a working set that does not fit shared memory: bitmap in global
+      // memory and the rest in shared memory if that fits, else all global
+      auto global_plan = [&](uint32_t lo, uint32_t hi, uint32_t dmax) {
+        Layout Ls = make_layout(dmax, levels, want_pv, 16, sbytes, true);
+        if (Ls.total <= smem_cap)
+          plans.push_back({lo, hi, Ls, WS_SYM_GLOBAL, 512});
+        else
+          plans.push_back({lo, hi, make_layout(dmax, levels, want_pv, 16, sbytes), WS_GLOBAL,
+                           512});
+      };
+      // heavy: d > SMEM_TIER_MAX
       uint32_t pos = 0;
       while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
       if (pos) {
-        plans.push_back({0, pos, make_layout(deg_at(0), levels, want_pv, 16, sbytes), true, 512});
+        global_plan(0, pos, deg_at(0));
         g.stats.sources_heavy = pos;
       }
       // shared-memory bins, sqrt(2) apart so each bin's footprint (and
@@ -1178,9 +1219,10 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
         if (end == pos) continue;
         const int nt = hi > 512 ? 512 : 256;
         Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes);
-        const bool gws = Lb.total > size_t(dev.smem_optin) - 1024;
-        if (gws) Lb = make_layout(deg_at(pos), levels, want_pv, 16, sbytes);
-        plans.push_back({pos, end, Lb, gws, gws ? 512 : nt});
+        if (Lb.total > smem_cap)
+          global_plan(pos, end, deg_at(pos));
+        else
+          plans.push_back({pos, end, Lb, WS_SMEM, nt});
         g.stats.sources_cta += end - pos;
         pos = end;
       }
@@ -1188,11 +1230,14 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
       // on aux[0])
       size_t arena = 0;
       for (const Plan& pl : plans)
-        if (pl.gws) {
-          const uint64_t fit = std::max<uint64_t>(1, budget / pl.L.total);
-          const uint64_t grid = std::min<uint64_t>(
-              {uint64_t(first[pl.hi] - first[pl.lo]), uint64_t(dev.sms) * 2, fit});
-          arena = std::max<size_t>(arena, grid * pl.L.total);
+        if (pl.gws != WS_SMEM) {
+          const size_t per = ws_global_bytes(pl.gws, pl.L);
+          const uint64_t fit = std::max<uint64_t>(1, budget / per);
+          // resident CTAs: <= 4 per SM at 512 threads (2 for all-global)
+          const uint64_t res = uint64_t(dev.sms) * (pl.gws == WS_SYM_GLOBAL ? 4 : 2);
+          const uint64_t grid =
+              std::min<uint64_t>({uint64_t(first[pl.hi] - first[pl.lo]), res, fit});
+          arena = std::max<size_t>(arena, grid * per);
         }
       if (arena) g.heavy.ensure(arena, &g.alloc);
       for (const Plan& pl : plans) {
@@ -1201,7 +1246,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
         a.nitems = first[pl.hi] - first[pl.lo];
         a.L = pl.L;
         a.work = work + wslot++;
-        cudaStream_t st = aux_stream(pl.gws);
+        cudaStream_t st = aux_stream(pl.gws != WS_SMEM);
         if (want_pv) {
           if (k <= 5)
             launch_cta<true, 0>(g, a, pl.gws, pl.nt, budget, st);
