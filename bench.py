@@ -335,6 +335,30 @@ def run_kcg(args):
                                    "cliques_per_s": tot2 / (cms / 1e3),
                                    "oriented_edges_per_s": g.m / (cms / 1e3)}
 
+    # downstream consumer of the per-vertex counts:
+    # approximate k-clique densest-subgraph peeling on the same handle
+    if world == 1:
+        h.rank(strat, eps, download=False)
+        h.direct(download=False)
+        h.peel_approx(k, 0.5)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        po = h.peel_approx(k, 0.5)
+        pms = (time.perf_counter() - t0) * 1e3
+        ent = {"ms": pms, "eps": 0.5, "rounds": po["rounds"], "best_round": po["best_round"],
+               "best_density": po["best_density"], "dense_vertices": len(po["dense_vertices"]),
+               "note": "per-vertex count + restricted recount per round, host-timed"}
+        pg = os.path.join(ROOT, "tests", "golden", "peel_configs.json")
+        if os.path.exists(pg):
+            ref = json.load(open(pg)).get(f"config{args.config}_k{k}_approx")
+            if ref:
+                ent["matches_reference"] = (
+                    ref["rounds"] == po["rounds"] and ref["best_round"] == po["best_round"]
+                    and ref["best_density"] == float(po["best_density"]).hex())
+                ent["reference_s"] = ref["ref_seconds"]
+                ent["reference_threads"] = ref["threads"]
+        secondary[f"peel_approx_k{k}"] = ent
+
     # e2e: the reference-facing C ABI with host buffers (pinned), H2D + D2H
     # inside the timed region
     e2e = None

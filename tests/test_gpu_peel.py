@@ -2,6 +2,9 @@
 kcg_peel_approx; kcg_peel.cu) against the reference's outputs in
 tests/golden/peel_cases.json and the reference's known answers
 (proj/tests/test_peeling.cpp).  Every call goes through the C ABI."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -119,3 +122,23 @@ def test_peel_approx_config2_properties():
         hs.direct(download=False)
         t_sub, _ = hs.count(4)
     assert t_sub / len(dense) == out["best_density"]
+
+
+def test_peel_config_goldens():
+    """Config-scale peeling against the reference's outcomes
+    (tests/golden/peel_configs.json, tools/make_peel_config_goldens.py)."""
+    path = os.path.join(peelcases.ROOT, "tests", "golden", "peel_configs.json")
+    gold = json.load(open(path))
+    for key, ent in sorted(gold.items()):
+        g = gen.load_config_graph(ent["config"], cache=False)
+        assert g.digest() == ent["graph_digest"], key
+        with oriented(g, ent["strategy"], ent["strategy_eps"]) as h:
+            out = h.peel_exact(ent["k"]) if ent["exact"] else h.peel_approx(ent["k"], ent["eps"])
+        assert out["rounds"] == ent["rounds"], key
+        assert str(out["total_cliques"]) == ent["total_cliques"], key
+        assert out["best_round"] == ent["best_round"], key
+        assert float(out["best_density"]).hex() == ent["best_density"], key
+        assert len(out["dense_vertices"]) == ent["num_dense"], key
+        assert f"{gen.digest_u32(out['dense_vertices']):016x}" == ent["dense_digest"], key
+        if ent["exact"]:
+            assert f"{gen.digest_u64(out['core']):016x}" == ent["core_digest"], key
