@@ -187,6 +187,28 @@ int kcg_peel_exact(kcg_graph* g, int k, kcg_peel_result* out, uint64_t* core,
 int kcg_peel_approx(kcg_graph* g, int k, double eps, kcg_peel_result* out,
                     uint32_t* dense_vertices);
 
+/* ---- Colour-sparsified approximate counting (SURVEY.md §8(f) row 3,
+ * proj/include/kclique/sampling.hpp:12-43). */
+
+/* SampleEstimate (sampling.hpp:12-19). */
+typedef struct kcg_sample_estimate {
+  int k;
+  uint64_t colors;
+  double p;            /* 1 / colors */
+  uint64_t sub_count;  /* exact count inside the sparsified graph */
+  double estimate;     /* sub_count * colors^(k-1) */
+  uint64_t seed;
+} kcg_sample_estimate;
+
+/* colorful_sparsify (sampling.cpp:28-40): *out is a new handle holding
+ * the subgraph of monochromatic edges.  KCG_EINVAL for colors < 1. */
+int kcg_colorful_sparsify(kcg_graph* g, uint64_t colors, uint64_t seed, kcg_graph** out);
+/* approx_count (sampling.cpp:42-57): sparsify, rank (strategy / eps /
+ * alpha_hat as kcg_rank), orient and count on the device.  KCG_EINVAL for
+ * k < 2 or colors < 1. */
+int kcg_approx_count(kcg_graph* g, int k, uint64_t colors, uint64_t seed, int strategy,
+                     double eps, uint64_t alpha_hat, kcg_sample_estimate* out);
+
 int kcg_timings(const kcg_graph* g, kcg_times* out);
 int kcg_last_count_stats(const kcg_graph* g, kcg_count_stats* out);
 /* Bytes of device memory the handle currently holds. */

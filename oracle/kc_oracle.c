@@ -515,3 +515,37 @@ out:
   free(round_of);
   return rc;
 }
+
+/* ---- colour sparsification ------------------- */
+
+static uint64_t kco_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+/* color_of, src/sampling.cpp:17-24 */
+uint64_t kco_color(uint64_t seed, uint32_t v, uint64_t colors) {
+  uint64_t h = kco_splitmix64(kco_splitmix64(seed) + 0x9e3779b97f4a7c15ULL * ((uint64_t)v + 1));
+  return (uint64_t)(((unsigned __int128)h * colors) >> 64);
+}
+
+/* colorful_sparsify, src/sampling.cpp:28-40: the monochromatic edges of the
+ * CSR, written as a CSR (out_off n+1, out_adj up to 2m).  Slices stay
+ * ascending, which is Graph::from_edges of the kept pairs. */
+int kco_sparsify(uint32_t n, const uint64_t* off, const uint32_t* adj, uint64_t colors,
+                 uint64_t seed, uint64_t* out_off, uint32_t* out_adj) {
+  if (colors < 1) return 1;
+  uint64_t* col = malloc(((size_t)n + 1) * sizeof(uint64_t));
+  if (!col) return 3;
+  for (uint32_t v = 0; v < n; v++) col[v] = colors == 1 ? 0 : kco_color(seed, v, colors);
+  out_off[0] = 0;
+  for (uint32_t v = 0; v < n; v++) {
+    out_off[v + 1] = out_off[v];
+    for (uint64_t p = off[v]; p < off[v + 1]; p++)
+      if (col[adj[p]] == col[v]) out_adj[out_off[v + 1]++] = adj[p];
+  }
+  free(col);
+  return 0;
+}

@@ -23,6 +23,7 @@
 #include "kclique/oracle.hpp"
 #include "kclique/orientation.hpp"
 #include "kclique/peeling.hpp"
+#include "kclique/sampling.hpp"
 
 using namespace kclique;
 
@@ -230,6 +231,32 @@ int ref_peel(void* g, void* dg, int k, int exact, double eps, uint64_t* res, dou
     if (dense && !o.dense_vertices.empty())
       std::memcpy(dense, o.dense_vertices.data(), o.dense_vertices.size() * 4);
   });
+}
+
+// colorful_sparsify (sampling.cpp:28-40) -> a new reference Graph
+int ref_colorful_sparsify(void* g, uint64_t colors, uint64_t seed, void** out) {
+  return guarded([&] {
+    *out = new Graph(colorful_sparsify(*static_cast<Graph*>(g), colors, seed));
+  });
+}
+
+// approx_count (sampling.cpp:42-57); res = {sub_count}, dres = {p, estimate}
+int ref_approx_count(void* g, int k, uint64_t colors, uint64_t seed, int strategy, double eps,
+                     uint64_t* sub_count, double* p, double* estimate) {
+  return guarded([&] {
+    OrientConfig oc;
+    oc.strategy = static_cast<OrientStrategy>(strategy);
+    oc.epsilon = eps;
+    SampleEstimate e = approx_count(*static_cast<Graph*>(g), k, colors, seed, oc);
+    *sub_count = e.sub_count;
+    *p = e.p;
+    *estimate = e.estimate;
+  });
+}
+
+double ref_analytic_variance(uint64_t true_count, double p, int k, const uint64_t* pairs,
+                             uint64_t npairs) {
+  return analytic_variance(true_count, p, k, std::span<const uint64_t>(pairs, npairs));
 }
 
 }  // extern "C"

@@ -23,6 +23,19 @@ inline void check(int rc) {
   throw std::runtime_error("kcg: " + msg);
 }
 
+// Adopts a device-built CSR (normalised on the GPU) as a host Graph.
+struct GraphAccess {
+  static Graph download(kcg_graph* h) {
+    Graph g;
+    g.n_ = kcg_num_vertices(h);
+    g.m_ = kcg_num_edges(h);
+    g.offsets_.assign(size_t(g.n_) + 1, 0);
+    g.neighbors_.resize(2 * g.m_);
+    check(kcg_graph_csr(h, g.offsets_.data(), g.neighbors_.data()));
+    return g;
+  }
+};
+
 class Handle {
  public:
   explicit Handle(kcg_graph* h) : h_(h) {}

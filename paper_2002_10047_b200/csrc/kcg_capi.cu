@@ -1,6 +1,7 @@
 // extern "C" surface of libkcg.so (include/kcg.h): handle lifecycle,
 // transfers, status-code mapping.  The compute phases live in
 // kcg_rank.cu, kcg_direct.cu and kcg_count.cu.
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -575,6 +576,50 @@ int kcg_peel_approx(kcg_graph* h, int k, double eps, kcg_peel_result* out,
     Graph& g = *G(h);
     g.times.d2h_bytes = 0;
     peel_result(peel(g, k, false, eps, nullptr), out, dense_vertices);
+  });
+}
+
+int kcg_colorful_sparsify(kcg_graph* h, uint64_t colors, uint64_t seed, kcg_graph** out) {
+  return guarded([&] {
+    if (!out) fail(KCG_EINVAL, "out is null");
+    *out = nullptr;
+    Graph& g = *G(h);
+    if (colors < 1) fail(KCG_EINVAL, "colors must be at least 1");
+    auto* d = new Graph();
+    try {
+      d->times = kcg_times{};
+      colorful_sparsify(g, *d, colors, seed);
+    } catch (...) {
+      delete d;
+      throw;
+    }
+    *out = reinterpret_cast<kcg_graph*>(d);
+  });
+}
+
+int kcg_approx_count(kcg_graph* h, int k, uint64_t colors, uint64_t seed, int strategy,
+                     double eps, uint64_t alpha_hat, kcg_sample_estimate* out) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (colors < 1) fail(KCG_EINVAL, "colors must be at least 1");
+    Graph sub;
+    colorful_sparsify(g, sub, colors, seed);
+    rank_graph(sub, strategy, eps, alpha_hat, nullptr);
+    sub.has_rank = true;
+    build_dag(sub, false);
+    const uint64_t total = count_cliques(sub, k, false);
+    g.times.count_ms = sub.times.count_ms;
+    g.times.count_kernel_ms = sub.times.count_kernel_ms;
+    g.times.launches += sub.times.launches;
+    if (out) {
+      out->k = k;
+      out->colors = colors;
+      out->p = 1.0 / double(colors);
+      out->sub_count = total;
+      out->estimate = double(total) * std::pow(double(colors), k - 1);
+      out->seed = seed;
+    }
   });
 }
 

@@ -187,6 +187,10 @@ void build_from_edges(Graph& g, uint32_t n, const uint32_t* us, const uint32_t* 
 void build_rmat(Graph& g, int scale, uint64_t samples, double a, double b, double c,
                 uint64_t seed, bool permute);
 
+// colour sparsification (kcg_sample.cu): dst receives the monochromatic
+// subgraph of src
+void colorful_sparsify(const Graph& src, Graph& dst, uint64_t colors, uint64_t seed);
+
 // peeling consumers of the per-vertex counts (kcg_peel.cu)
 struct UpdateOut {
   uint64_t removed = 0;

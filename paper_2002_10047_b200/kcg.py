@@ -32,7 +32,8 @@ EXPORTED = [
     "kcg_count", "kcg_per_vertex_device", "kcg_pipeline", "kcg_timings",
     "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
     "kcg_stream", "kcg_update_counts", "kcg_peel_exact", "kcg_peel_approx",
-    "kcg_graph_from_edges", "kcg_graph_rmat", "kcg_graph_csr",
+    "kcg_graph_from_edges", "kcg_graph_rmat", "kcg_graph_csr", "kcg_colorful_sparsify",
+    "kcg_approx_count",
 ]
 
 
@@ -48,6 +49,15 @@ class KcgOutOfMemory(KcgError, MemoryError):
 
 class KcgLogicError(KcgError):
     """The reference's std::logic_error cases (peeling)."""
+
+
+class SampleEstimate(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int), ("colors", ctypes.c_uint64), ("p", ctypes.c_double),
+                ("sub_count", ctypes.c_uint64), ("estimate", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class PeelResult(ctypes.Structure):
@@ -125,6 +135,9 @@ def lib():
         L.kcg_graph_rmat.argtypes = [ctypes.c_int, u64, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, u64, ctypes.c_int, P(vp)]
         L.kcg_graph_csr.argtypes = [vp, vp, vp]
+        L.kcg_colorful_sparsify.argtypes = [vp, u64, u64, P(vp)]
+        L.kcg_approx_count.argtypes = [vp, ctypes.c_int, u64, u64, ctypes.c_int, ctypes.c_double,
+                                       u64, P(SampleEstimate)]
         L.kcg_update_counts.argtypes = [vp, ctypes.c_int, vp, vp, u64, vp, P(u64), vp, P(u64)]
         L.kcg_peel_exact.argtypes = [vp, ctypes.c_int, P(PeelResult), vp, vp]
         L.kcg_peel_approx.argtypes = [vp, ctypes.c_int, ctypes.c_double, P(PeelResult), vp]
@@ -322,6 +335,18 @@ class DeviceGraph:
 
     def synchronize(self):
         _check(lib().kcg_synchronize(self._h))
+
+    # ---- colour sparsification (kcg_sample.cu; sampling.hpp:21-36) ----
+    def colorful_sparsify(self, colors, seed) -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        _check(lib().kcg_colorful_sparsify(self._h, int(colors), int(seed), ctypes.byref(h)))
+        return DeviceGraph(h)
+
+    def approx_count(self, k, colors, seed, strategy=0, eps=1.0, alpha_hat=0) -> dict:
+        est = SampleEstimate()
+        _check(lib().kcg_approx_count(self._h, int(k), int(colors), int(seed), int(strategy),
+                                      float(eps), int(alpha_hat), ctypes.byref(est)))
+        return est.as_dict()
 
     # ---- peeling (kcg_peel.cu; peeling.hpp:58-92) ----
     def update_counts(self, k, counts, batch, peeled):

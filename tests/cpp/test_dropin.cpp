@@ -2,7 +2,7 @@
 // linked against libkclique_b200.so (which runs on the B200), exercising
 // the reference API the way the reference's own unit tests do
 // (proj/tests/test_counting.cpp, test_orientation.cpp, test_graph.cpp,
-// test_peeling.cpp, test_bucket_queue.cpp).
+// test_peeling.cpp, test_bucket_queue.cpp, test_sampling.cpp).
 // The expected values are the reference's known answers; the brute-force
 // checker below is an independent exhaustive enumeration.
 //
@@ -22,6 +22,7 @@
 #include "kclique/graph.hpp"
 #include "kclique/orientation.hpp"
 #include "kclique/peeling.hpp"
+#include "kclique/sampling.hpp"
 
 using namespace kclique;
 
@@ -478,6 +479,37 @@ void case_peel() {
   }
 }
 
+// ---- sampling (proj/tests/test_sampling.cpp) ----
+void case_sampling() {
+  Graph g = gnp(30, 0.3, 5);
+  CHECK(colorful_sparsify(g, 1, 42) == g);
+  SampleEstimate est = approx_count(g, 3, 1, 42);
+  CHECK(est.p == 1.0 && est.sub_count == brute(g, 3).total);
+  CHECK(est.estimate == double(est.sub_count));
+  for (uint64_t seed : {1u, 2u, 3u}) {
+    Graph h = gnp(40, 0.25, seed + 60);
+    for (uint32_t colors : {2u, 3u, 5u}) {
+      Graph sub = colorful_sparsify(h, colors, seed);
+      CHECK(sub.num_vertices() == h.num_vertices() && sub.num_edges() <= h.num_edges());
+      CHECK(sub == colorful_sparsify(h, colors, seed));
+      for (VertexId v = 0; v < sub.num_vertices(); v++)
+        for (VertexId u : sub.neighbors(v)) CHECK(h.has_edge(v, u));
+      // exact count of the sparsified graph == approx_count's sub_count
+      CHECK(approx_count(h, 3, colors, seed).sub_count == brute(sub, 3).total);
+    }
+  }
+  Graph g24 = gnp(24, 0.4, 99);
+  SampleEstimate e4 = approx_count(g24, 4, 3, 7);
+  CHECK(e4.k == 4 && e4.colors == 3 && e4.p == 1.0 / 3.0);
+  CHECK(e4.estimate == double(e4.sub_count) * 27.0);
+  CHECK(approx_count(g24, 4, 3, 7).estimate == e4.estimate);
+  CHECK_THROWS_AS(colorful_sparsify(complete(4), 0, 1), std::invalid_argument);
+  CHECK_THROWS_AS(approx_count(complete(4), 1, 2, 1), std::invalid_argument);
+  std::vector<uint64_t> none(3, 0);
+  CHECK(analytic_variance(10, 1.0, 3, none) == 0.0);
+  CHECK(analytic_variance(1, 0.5, 3, none) == 3.0);
+}
+
 }  // namespace
 
 int main() {
@@ -501,6 +533,7 @@ int main() {
       {"bucket queue", case_bucket_queue},
       {"update_counts", case_update_counts},
       {"peel_exact / peel_approx", case_peel},
+      {"colour sparsification / approx_count", case_sampling},
   };
   for (auto& c : cases) {
     int before = g_fail;

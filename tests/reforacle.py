@@ -73,6 +73,13 @@ class Ref:
         L.ref_set_threads.argtypes = [ctypes.c_int]
         L.ref_update_counts.argtypes = [vp, vp, ctypes.c_int, vp, vp, ctypes.c_uint64, vp,
                                         P(ctypes.c_uint64), vp, P(ctypes.c_uint64)]
+        L.ref_colorful_sparsify.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, P(vp)]
+        L.ref_approx_count.argtypes = [vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.c_int, ctypes.c_double, P(ctypes.c_uint64),
+                                       P(ctypes.c_double), P(ctypes.c_double)]
+        L.ref_analytic_variance.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, vp,
+                                            ctypes.c_uint64]
+        L.ref_analytic_variance.restype = ctypes.c_double
         L.ref_peel.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, vp,
                                P(ctypes.c_double), vp, vp, P(ctypes.c_double)]
         self.L = L
@@ -178,6 +185,26 @@ class Ref:
                "update_counts")
         return int(removed.value), changed[:nch.value].copy()
 
+    def colorful_sparsify(self, h, n, colors, seed):
+        """Returns the sparsified reference Graph as (offsets, adjacency)."""
+        out = ctypes.c_void_p()
+        _check(self.L.ref_colorful_sparsify(h, colors, seed, ctypes.byref(out)), "sparsify")
+        csr = self.graph_csr(out, n)
+        self.graph_destroy(out)
+        return csr
+
+    def approx_count(self, h, k, colors, seed, strategy=0, eps=1.0):
+        sc = ctypes.c_uint64(0)
+        p = ctypes.c_double(0)
+        e = ctypes.c_double(0)
+        _check(self.L.ref_approx_count(h, k, colors, seed, strategy, eps, ctypes.byref(sc),
+                                       ctypes.byref(p), ctypes.byref(e)), "approx_count")
+        return {"sub_count": int(sc.value), "p": p.value, "estimate": e.value}
+
+    def analytic_variance(self, true_count, p, k, pairs):
+        a = _arr(pairs, np.uint64)
+        return self.L.ref_analytic_variance(true_count, p, k, a.ctypes.data, len(a))
+
     def peel(self, h, dg, n, k, exact, eps=0.5):
         res = np.zeros(4, np.uint64)
         dens = ctypes.c_double(0)
@@ -222,6 +249,8 @@ class Port:
         L.kco_update_counts.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, vp, vp,
                                         ctypes.c_uint64, vp, P(ctypes.c_uint64), vp,
                                         P(ctypes.c_uint64)]
+        L.kco_sparsify.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_uint64, ctypes.c_uint64,
+                                   vp, vp]
         L.kco_peel.argtypes = [ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.c_int,
                                ctypes.c_double, vp, P(ctypes.c_double), vp, vp]
         self.L = L
@@ -300,3 +329,11 @@ class Port:
         if exact:
             out["core"] = core[:g.n].copy()
         return out
+
+    def sparsify(self, g, colors, seed):
+        """colorful_sparsify restatement -> (offsets, adjacency)."""
+        off = np.zeros(g.n + 1, np.uint64)
+        adj = np.zeros(max(2 * g.m, 1), np.uint32)
+        _check(self.L.kco_sparsify(g.n, g.offsets.ctypes.data, g.adj.ctypes.data, colors, seed,
+                                   off.ctypes.data, adj.ctypes.data), "sparsify")
+        return off, adj[:int(off[-1])]
