@@ -153,6 +153,15 @@ int kcg_per_vertex_device(kcg_graph* g, const uint64_t** d_per_vertex);
 int kcg_pipeline(kcg_graph* g, int strategy, double eps, uint64_t alpha_hat,
                  int k, uint64_t* total, uint64_t* per_vertex);
 
+/* list_cliques (counting.hpp:42-49, counting.cpp:214-217) on the device:
+ * every k-clique exactly once, vertices in ascending rank, delivered to
+ * `fn` in batches of at most `batch` cliques (0: 2^24) as count * k vertex
+ * ids (row-major).  A non-zero return from fn aborts with KCG_ERUNTIME.
+ * *total receives the clique count.  KCG_EINVAL for k < 2 or k > 33. */
+typedef int (*kcg_clique_fn)(const uint32_t* cliques, uint64_t count, int k, void* user);
+int kcg_list_cliques(kcg_graph* g, int k, uint64_t batch, kcg_clique_fn fn, void* user,
+                     uint64_t* total);
+
 /* ---- Peeling: consumers of the per-vertex counts (SURVEY.md §8(f) row 1,
  * proj/include/kclique/peeling.hpp:59-92).  The handle must hold the
  * undirected graph (kcg_graph_create) and a ranking (kcg_rank or

@@ -1,6 +1,8 @@
 // Drop-in counting entry points (include/kclique/counting.hpp): the
 // DirectedGraph is adopted by a device handle (kcg_dag_create, which
 // relabels it by rank on the GPU) and counted by kcg_count.
+#include <exception>
+
 #include "kcg_handle.hpp"
 #include "kclique/counting.hpp"
 
@@ -34,11 +36,31 @@ CliqueCounts count_per_vertex(const DirectedGraph& dg, int k, const CountConfig&
 CliqueCounts list_cliques(const DirectedGraph& dg, int k, const CountConfig&,
                           const CliqueCallback& emit) {
   if (k < 2) throw std::invalid_argument("k must be at least 2");
-  (void)dg;
-  (void)emit;
-  // Device-side emission is SURVEY.md §8(f) row 3 ("next"); refuse loudly
-  // rather than enumerate on the CPU.
-  throw std::runtime_error("list_cliques: clique emission is not implemented on the B200 path");
+  CliqueCounts out;
+  out.k = k;
+  if (dg.num_vertices() == 0) return out;
+  auto h = b200::Handle::adopt(dg);
+  // cliques arrive in device batches; each is reported in ascending rank
+  // (an exception from the callback aborts the listing and is rethrown)
+  struct Ctx {
+    const CliqueCallback* emit;
+    std::exception_ptr err;
+  } ctx{&emit, nullptr};
+  auto fn = [](const uint32_t* c, uint64_t count, int kk, void* user) -> int {
+    auto* cx = static_cast<Ctx*>(user);
+    try {
+      for (uint64_t i = 0; i < count; i++)
+        (*cx->emit)(std::span<const VertexId>(c + i * uint64_t(kk), size_t(kk)));
+    } catch (...) {
+      cx->err = std::current_exception();
+      return 1;
+    }
+    return 0;
+  };
+  const int rc = kcg_list_cliques(h.get(), k, 0, fn, &ctx, &out.total);
+  if (ctx.err) std::rethrow_exception(ctx.err);
+  b200::check(rc);
+  return out;
 }
 
 }  // namespace kclique

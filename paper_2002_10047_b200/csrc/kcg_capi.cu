@@ -623,6 +623,16 @@ int kcg_approx_count(kcg_graph* h, int k, uint64_t colors, uint64_t seed, int st
   });
 }
 
+int kcg_list_cliques(kcg_graph* h, int k, uint64_t batch, kcg_clique_fn fn, void* user,
+                     uint64_t* total) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    g.times.d2h_bytes = 0;
+    const uint64_t t = list_cliques(g, k, batch, fn, user);
+    if (total) *total = t;
+  });
+}
+
 int kcg_timings(const kcg_graph* h, kcg_times* out) {
   return guarded([&] {
     if (!out) fail(KCG_EINVAL, "null out pointer");

@@ -187,6 +187,9 @@ void build_from_edges(Graph& g, uint32_t n, const uint32_t* us, const uint32_t* 
 void build_rmat(Graph& g, int scale, uint64_t samples, double a, double b, double c,
                 uint64_t seed, bool permute);
 
+// clique listing (kcg_list.cu); returns the clique count
+uint64_t list_cliques(Graph& g, int k, uint64_t batch, kcg_clique_fn fn, void* user);
+
 // colour sparsification (kcg_sample.cu): dst receives the monochromatic
 // subgraph of src
 void colorful_sparsify(const Graph& src, Graph& dst, uint64_t colors, uint64_t seed);

@@ -33,7 +33,7 @@ EXPORTED = [
     "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
     "kcg_stream", "kcg_update_counts", "kcg_peel_exact", "kcg_peel_approx",
     "kcg_graph_from_edges", "kcg_graph_rmat", "kcg_graph_csr", "kcg_colorful_sparsify",
-    "kcg_approx_count",
+    "kcg_approx_count", "kcg_list_cliques",
 ]
 
 
@@ -49,6 +49,10 @@ class KcgOutOfMemory(KcgError, MemoryError):
 
 class KcgLogicError(KcgError):
     """The reference's std::logic_error cases (peeling)."""
+
+
+CLIQUE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint64,
+                             ctypes.c_int, ctypes.c_void_p)
 
 
 class SampleEstimate(ctypes.Structure):
@@ -135,6 +139,7 @@ def lib():
         L.kcg_graph_rmat.argtypes = [ctypes.c_int, u64, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, u64, ctypes.c_int, P(vp)]
         L.kcg_graph_csr.argtypes = [vp, vp, vp]
+        L.kcg_list_cliques.argtypes = [vp, ctypes.c_int, u64, CLIQUE_FN, vp, P(u64)]
         L.kcg_colorful_sparsify.argtypes = [vp, u64, u64, P(vp)]
         L.kcg_approx_count.argtypes = [vp, ctypes.c_int, u64, u64, ctypes.c_int, ctypes.c_double,
                                        u64, P(SampleEstimate)]
@@ -335,6 +340,23 @@ class DeviceGraph:
 
     def synchronize(self):
         _check(lib().kcg_synchronize(self._h))
+
+    def list_cliques(self, k, batch=0):
+        """list_cliques: (total, array[total, k] of vertex ids, each row in
+        ascending rank)."""
+        parts = []
+
+        def cb(ptr, count, kk, _user):
+            parts.append(np.ctypeslib.as_array(ptr, shape=(int(count) * kk,)).copy()
+                         .reshape(-1, kk))
+            return 0
+
+        fn = CLIQUE_FN(cb)
+        total = ctypes.c_uint64(0)
+        _check(lib().kcg_list_cliques(self._h, int(k), int(batch), fn, None,
+                                      ctypes.byref(total)))
+        arr = np.concatenate(parts) if parts else np.zeros((0, k), np.uint32)
+        return int(total.value), arr
 
     # ---- colour sparsification (kcg_sample.cu; sampling.hpp:21-36) ----
     def colorful_sparsify(self, colors, seed) -> "DeviceGraph":

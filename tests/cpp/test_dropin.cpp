@@ -479,6 +479,43 @@ void case_peel() {
   }
 }
 
+// ---- list_cliques (proj/tests/test_counting.cpp:103-128) ----
+void case_list_cliques() {
+  for (uint64_t seed = 0; seed < 6; seed++) {
+    Graph g = gnp(16, 0.55, seed + 900);
+    for (auto s : {OrientStrategy::degree, OrientStrategy::original}) {
+      Ranking r = make_ranking(g, {s, 1.0, {}});
+      DirectedGraph dg = direct_by_ranking(g, r);
+      for (int k : {2, 3, 4, 5}) {
+        std::vector<std::vector<VertexId>> got;
+        CliqueCounts c = list_cliques(dg, k, {}, [&](std::span<const VertexId> cl) {
+          CHECK(cl.size() == size_t(k));
+          for (size_t i = 1; i < cl.size(); i++) CHECK(r.rank_of(cl[i - 1]) < r.rank_of(cl[i]));
+          std::vector<VertexId> ids(cl.begin(), cl.end());
+          std::sort(ids.begin(), ids.end());
+          for (size_t i = 0; i < ids.size(); i++)
+            for (size_t j = i + 1; j < ids.size(); j++) CHECK(g.has_edge(ids[i], ids[j]));
+          got.push_back(std::move(ids));
+        });
+        CHECK(c.total == brute(g, k).total);
+        CHECK(got.size() == c.total);
+        std::sort(got.begin(), got.end());
+        CHECK(std::adjacent_find(got.begin(), got.end()) == got.end());
+      }
+    }
+  }
+  CHECK_THROWS_AS(list_cliques(oriented(complete(4)), 1, {}, [](std::span<const VertexId>) {}),
+                  std::invalid_argument);
+  bool thrown = false;
+  try {
+    list_cliques(oriented(complete(6)), 3, {},
+                 [](std::span<const VertexId>) { throw std::out_of_range("stop"); });
+  } catch (const std::out_of_range&) {
+    thrown = true;
+  }
+  CHECK(thrown);
+}
+
 // ---- sampling (proj/tests/test_sampling.cpp) ----
 void case_sampling() {
   Graph g = gnp(30, 0.3, 5);
@@ -534,6 +571,7 @@ int main() {
       {"update_counts", case_update_counts},
       {"peel_exact / peel_approx", case_peel},
       {"colour sparsification / approx_count", case_sampling},
+      {"list_cliques", case_list_cliques},
   };
   for (auto& c : cases) {
     int before = g_fail;
