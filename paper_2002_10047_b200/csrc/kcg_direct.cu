@@ -23,14 +23,25 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Hubs (undirected degree > kHubDeg) are listed by the warp kernels and
+// handled by one CTA each (outdeg_hub_kernel, fill_hub_kernel): a single warp
+// walking a 50k-entry slice with dependent gathers was the long tail of
+// both passes on the skewed configs.
+constexpr uint32_t kHubDeg = 2048;
+
 __global__ void outdeg_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                               const uint32_t* __restrict__ rank, uint32_t n,
-                              uint64_t* __restrict__ outdeg, uint64_t* __restrict__ rdeg) {
+                              uint64_t* __restrict__ outdeg, uint64_t* __restrict__ rdeg,
+                              uint32_t* __restrict__ hubs, unsigned* __restrict__ nhubs) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n;
        u += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     const uint32_t ru = rank[u];
     const uint64_t b = off[u], e = off[u + 1];
+    if (e - b > kHubDeg) {
+      if (lane == 0) hubs[atomicAdd(nhubs, 1u)] = uint32_t(u);
+      continue;
+    }
     uint32_t c = 0;
     for (uint64_t p0 = b; p0 < e; p0 += 32) {
       uint64_t p = p0 + lane;
@@ -41,6 +52,37 @@ __global__ void outdeg_kernel(const uint64_t* __restrict__ off, const uint32_t* 
       if (outdeg) outdeg[u] = c;
       rdeg[ru] = c;
     }
+  }
+}
+
+// One CTA per hub: the slice is read 4 x 512 entries per step (loads in
+// flight), out-neighbours counted with a block reduction.
+__global__ void __launch_bounds__(512)
+    outdeg_hub_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                      const uint32_t* __restrict__ rank, const uint32_t* __restrict__ hubs,
+                      const unsigned* __restrict__ nhubs, uint64_t* __restrict__ outdeg,
+                      uint64_t* __restrict__ rdeg) {
+  typedef cub::BlockReduce<uint32_t, 512> Red;
+  __shared__ typename Red::TempStorage tmp;
+  const unsigned nh = *nhubs;
+  for (unsigned hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const uint32_t u = hubs[hi];
+    const uint32_t ru = rank[u];
+    const uint64_t b = off[u], e = off[u + 1];
+    uint32_t c = 0;
+    for (uint64_t p0 = b + threadIdx.x; p0 < e; p0 += 4 * 512) {
+      uint32_t a[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) a[j] = p0 + j * 512 < e ? adj[p0 + j * 512] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < 4; j++) c += a[j] != 0xffffffffu && rank[a[j]] > ru;
+    }
+    c = Red(tmp).Sum(c);
+    if (threadIdx.x == 0) {
+      if (outdeg) outdeg[u] = c;
+      rdeg[ru] = c;
+    }
+    __syncthreads();
   }
 }
 
@@ -75,6 +117,7 @@ __global__ void __launch_bounds__(256)
        u += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     const uint32_t ru = rank[u];
     const uint64_t b = off[u], e = off[u + 1];
+    if (e - b > kHubDeg) continue;  // fill_hub_kernel
     uint64_t wid = dag_adj ? dag_off[u] : 0;
     const uint64_t wr0 = rdag_off[ru];
     const uint32_t dout = uint32_t(rdag_off[ru + 1] - wr0);
@@ -115,6 +158,61 @@ __global__ void __launch_bounds__(256)
       else
         long_list[n - 1 - atomicAdd(&nlong[1], 1u)] = ru;
     }
+  }
+}
+
+// fill_kernel for the hubs: one CTA each, ordered compaction of 512
+// entries per step with a block scan; the relabelled slice goes to the
+// sort lists like the warp path's (<= 32 targets: sorted here by warp 0).
+__global__ void __launch_bounds__(512)
+    fill_hub_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                    const uint32_t* __restrict__ rank, uint32_t n,
+                    const uint32_t* __restrict__ hubs, const unsigned* __restrict__ nhubs,
+                    const uint64_t* __restrict__ dag_off, uint32_t* __restrict__ dag_adj,
+                    const uint64_t* __restrict__ rdag_off, uint32_t* __restrict__ rdag_adj,
+                    uint32_t* __restrict__ long_list, unsigned* __restrict__ nlong) {
+  typedef cub::BlockScan<uint32_t, 512> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const unsigned nh = *nhubs;
+  for (unsigned hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const uint32_t u = hubs[hi];
+    const uint32_t ru = rank[u];
+    const uint64_t b = off[u], e = off[u + 1];
+    const uint64_t wid = dag_adj ? dag_off[u] : 0;
+    const uint64_t wr0 = rdag_off[ru];
+    const uint32_t dout = uint32_t(rdag_off[ru + 1] - wr0);
+    uint32_t got = 0;
+    for (uint64_t p0 = b; p0 < e && got < dout; p0 += 512) {
+      const uint64_t p = p0 + threadIdx.x;
+      uint32_t v = 0, rv = 0, out = 0;
+      if (p < e) {
+        v = adj[p];
+        rv = rank[v];
+        out = rv > ru;
+      }
+      uint32_t at, tot;
+      Scan(tmp).ExclusiveSum(out, at, tot);
+      if (out) {
+        if (dag_adj) dag_adj[wid + got + at] = v;
+        rdag_adj[wr0 + got + at] = rv;
+      }
+      got += tot;
+      __syncthreads();
+    }
+    if (dout <= 32) {
+      __syncthreads();
+      if (threadIdx.x < 32 && dout) {
+        uint32_t x = threadIdx.x < dout ? rdag_adj[wr0 + threadIdx.x] : 0xffffffffu;
+        x = warp_bitonic_sort(x, threadIdx.x);
+        if (threadIdx.x < dout) rdag_adj[wr0 + threadIdx.x] = x;
+      }
+    } else if (threadIdx.x == 0) {
+      if (dout <= kMidSortL)
+        long_list[atomicAdd(&nlong[0], 1u)] = ru;
+      else
+        long_list[n - 1 - atomicAdd(&nlong[1], 1u)] = ru;
+    }
+    __syncthreads();
   }
 }
 
@@ -281,20 +379,32 @@ void build_dag(Graph& g, bool want_id_dag) {
   KCG_CUDA(cudaMemsetAsync(rdeg + n, 0, 8, g.stream));
   if (odeg) KCG_CUDA(cudaMemsetAsync(odeg + n, 0, 8, g.stream));
   unsigned grid = blocks_for(uint64_t(n) * 32, kThreads, 148u * 64u);
-  if (n) outdeg_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n,
-                                                        odeg, rdeg);
-  KCG_LAUNCHED(g);
+  uint32_t* lists = reinterpret_cast<uint32_t*>(g.scratch3.ensure(size_t(n) * 8 + 64, &g.alloc));
+  uint32_t* hubs = lists + n;
+  unsigned* cnt = reinterpret_cast<unsigned*>(g.counters.ensure(8, &g.alloc) + 3);
+  KCG_CUDA(cudaMemsetAsync(cnt, 0, 12, g.stream));  // [0,1] sort lists, [2] hubs
+  if (n) {
+    outdeg_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n, odeg,
+                                                   rdeg, hubs, cnt + 2);
+    KCG_LAUNCHED(g);
+    outdeg_hub_kernel<<<148, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, hubs,
+                                                 cnt + 2, odeg, rdeg);
+    KCG_LAUNCHED(g);
+  }
   exclusive_scan_u64(g, rdeg, g.rdag_off.p, size_t(n) + 1);
   if (odeg) exclusive_scan_u64(g, odeg, g.dag_off.p, size_t(n) + 1);
-  uint32_t* lists = reinterpret_cast<uint32_t*>(g.scratch3.ensure(size_t(n) * 4 + 64, &g.alloc));
-  unsigned* cnt = reinterpret_cast<unsigned*>(g.counters.ensure(4, &g.alloc) + 3);
-  KCG_CUDA(cudaMemsetAsync(cnt, 0, 8, g.stream));
-  if (n)
+  if (n) {
     fill_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n,
                                                  want_id_dag ? g.dag_off.p : nullptr,
                                                  want_id_dag ? g.dag_adj.p : nullptr,
                                                  g.rdag_off.p, g.rdag_adj.p, lists, cnt);
-  KCG_LAUNCHED(g);
+    KCG_LAUNCHED(g);
+    fill_hub_kernel<<<148, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n, hubs,
+                                               cnt + 2, want_id_dag ? g.dag_off.p : nullptr,
+                                               want_id_dag ? g.dag_adj.p : nullptr, g.rdag_off.p,
+                                               g.rdag_adj.p, lists, cnt);
+    KCG_LAUNCHED(g);
+  }
   max_out_degree(g, rdeg);
   unsigned hcnt[2] = {0, 0};
   KCG_CUDA(cudaMemcpyAsync(hcnt, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
