@@ -78,17 +78,27 @@ __global__ void invert_kernel(const uint32_t* __restrict__ rank, uint32_t n,
 }
 
 // Degree decrements for the survivors of a BE / GP round: one warp per
-// batch vertex, lanes stride its adjacency.
+// batch vertex, lanes stride its adjacency.  Hubs (degree > kHubDeg) are
+// only listed here and spread over the whole grid by decrement_hub_kernel
+// (one warp walking a 50k-entry slice was the tail of the round).
+constexpr uint64_t kHubDeg = 2048;
+
 __global__ void decrement_kernel(const uint32_t* __restrict__ batch, uint32_t nb,
                                  const uint64_t* __restrict__ off,
                                  const uint32_t* __restrict__ adj,
                                  const uint8_t* __restrict__ alive,
-                                 uint32_t* __restrict__ deg) {
+                                 uint32_t* __restrict__ deg, uint32_t* __restrict__ hubs,
+                                 unsigned* __restrict__ nhubs) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nb;
        w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     uint32_t v = batch[w];
-    for (uint64_t p = off[v] + lane; p < off[v + 1]; p += 32) {
+    const uint64_t b = off[v], e = off[v + 1];
+    if (e - b > kHubDeg) {
+      if (lane == 0) hubs[atomicAdd(nhubs, 1u)] = v;
+      continue;
+    }
+    for (uint64_t p = b + lane; p < e; p += 32) {
       uint32_t u = adj[p];
       if (alive[u] == 1) atomicSub(&deg[u], 1u);
     }
@@ -99,30 +109,72 @@ __global__ void decrement_kernel(const uint32_t* __restrict__ batch, uint32_t nb
 // round's batch.  Reproduces the reference's sequential batch walk
 // (orientation.cpp:146-154): an edge to a survivor is removed once, an
 // intra-batch edge once (by its lower-id endpoint).
+__device__ __forceinline__ void arb_edge(uint32_t v, uint32_t u, const uint8_t* alive,
+                                         uint32_t* deg, unsigned long long& mine) {
+  const uint8_t a = alive[u];
+  if (a == 1) {
+    atomicSub(&deg[u], 1u);
+    mine++;
+  } else if (a == 2 && u > v) {
+    mine++;
+  }
+}
+
 __global__ void arb_decrement_kernel(const uint32_t* __restrict__ batch, uint32_t nb,
                                      const uint64_t* __restrict__ off,
                                      const uint32_t* __restrict__ adj,
                                      const uint8_t* __restrict__ alive,
                                      uint32_t* __restrict__ deg,
-                                     unsigned long long* __restrict__ removed) {
+                                     unsigned long long* __restrict__ removed,
+                                     uint32_t* __restrict__ hubs, unsigned* __restrict__ nhubs) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long mine = 0;
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nb;
        w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     uint32_t v = batch[w];
-    for (uint64_t p = off[v] + lane; p < off[v + 1]; p += 32) {
-      uint32_t u = adj[p];
-      uint8_t a = alive[u];
-      if (a == 1) {
-        atomicSub(&deg[u], 1u);
-        mine++;
-      } else if (a == 2 && u > v) {
-        mine++;
-      }
+    const uint64_t b = off[v], e = off[v + 1];
+    if (e - b > kHubDeg) {
+      if (lane == 0) hubs[atomicAdd(nhubs, 1u)] = v;
+      continue;
     }
+    for (uint64_t p = b + lane; p < e; p += 32) arb_edge(v, adj[p], alive, deg, mine);
   }
   for (int s = 16; s; s >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, s);
   if (lane == 0 && mine) atomicAdd(removed, mine);
+}
+
+// The listed hubs: one CTA per hub, four loads in flight per thread.
+// ARB: the arboricity-round semantics of arb_decrement_kernel.
+template <bool ARB>
+__global__ void __launch_bounds__(256)
+    decrement_hub_kernel(const uint32_t* __restrict__ hubs, const unsigned* __restrict__ nhubs,
+                         const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                         const uint8_t* __restrict__ alive, uint32_t* __restrict__ deg,
+                         unsigned long long* __restrict__ removed) {
+  const unsigned nh = *nhubs;
+  unsigned long long mine = 0;
+  for (unsigned h = blockIdx.x; h < nh; h += gridDim.x) {
+    const uint32_t v = hubs[h];
+    const uint64_t e = off[v + 1];
+    for (uint64_t p0 = off[v] + threadIdx.x; p0 < e; p0 += 4 * 256) {
+      uint32_t u[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) u[j] = p0 + j * 256 < e ? adj[p0 + j * 256] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (u[j] == 0xffffffffu) continue;
+        if constexpr (ARB) {
+          arb_edge(v, u[j], alive, deg, mine);
+        } else {
+          if (alive[u[j]] == 1) atomicSub(&deg[u[j]], 1u);
+        }
+      }
+    }
+  }
+  if constexpr (ARB) {
+    for (int s = 16; s; s >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, s);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(removed, mine);
+  }
 }
 
 __global__ void kill_kernel(const uint32_t* __restrict__ batch, uint32_t nb,
@@ -235,7 +287,8 @@ struct Peel {
   uint32_t* pos;
   uint64_t* keys;
   uint64_t* keys2;
-  unsigned long long* ctr;
+  uint32_t* hubs;
+  unsigned long long* ctr;  // [0] removed edges, [4] (as u32) hub count
 };
 
 Peel peel_state(Graph& g, bool with_keys) {
@@ -247,7 +300,8 @@ Peel peel_state(Graph& g, bool with_keys) {
     return at;
   };
   size_t o_wdeg = carve(n * 4), o_alive = carve(n), o_rem = carve(n * 4),
-         o_rem2 = carve(n * 4), o_batch = carve(n * 4), o_pos = carve(n * 4 + 4);
+         o_rem2 = carve(n * 4), o_batch = carve(n * 4), o_pos = carve(n * 4 + 4),
+         o_hubs = carve(n * 4 + 4);
   size_t o_keys = with_keys ? carve(n * 8) : 0, o_keys2 = with_keys ? carve(n * 8) : 0;
   unsigned char* base = g.scratch2.ensure(bytes + 256, &g.alloc);
   Peel p;
@@ -259,6 +313,7 @@ Peel peel_state(Graph& g, bool with_keys) {
   p.pos = reinterpret_cast<uint32_t*>(base + o_pos);
   p.keys = with_keys ? reinterpret_cast<uint64_t*>(base + o_keys) : nullptr;
   p.keys2 = with_keys ? reinterpret_cast<uint64_t*>(base + o_keys2) : nullptr;
+  p.hubs = reinterpret_cast<uint32_t*>(base + o_hubs);
   p.ctr = g.counters.ensure(8, &g.alloc);
   if (n) {
     KCG_CUDA(cudaMemcpyAsync(p.wdeg, g.deg.p, n * 4, cudaMemcpyDeviceToDevice, g.stream));
@@ -267,6 +322,18 @@ Peel peel_state(Graph& g, bool with_keys) {
     KCG_LAUNCHED(g);
   }
   return p;
+}
+
+// Survivor degree decrements for batch P.batch[0..nb) (BE / GP rounds).
+void decrement(Graph& g, Peel& P, uint32_t nb) {
+  unsigned* nh = reinterpret_cast<unsigned*>(P.ctr + 4);
+  KCG_CUDA(cudaMemsetAsync(nh, 0, 4, g.stream));
+  decrement_kernel<<<blocks_for(uint64_t(nb) * 32, kThreads), kThreads, 0, g.stream>>>(
+      P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, P.hubs, nh);
+  KCG_LAUNCHED(g);
+  decrement_hub_kernel<false><<<148 * 4, kThreads, 0, g.stream>>>(
+      P.hubs, nh, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, nullptr);
+  KCG_LAUNCHED(g);
 }
 
 // Ordered flag scan: pos[i] = #flags before i; returns the batch size.
@@ -341,9 +408,7 @@ uint64_t rank_be(Graph& g, double eps, uint64_t alpha_hat) {
     split_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(
         flag, P.rem, nrem, P.pos, P.batch, P.rem2, P.alive, 0, g.rank.p, placed);
     KCG_LAUNCHED(g);
-    decrement_kernel<<<blocks_for(uint64_t(nb) * 32, kThreads), kThreads, 0, g.stream>>>(
-        P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg);
-    KCG_LAUNCHED(g);
+    decrement(g, P, nb);
     std::swap(P.rem, P.rem2);
     nrem -= nb;
     placed += nb;
@@ -377,9 +442,7 @@ uint64_t rank_gp(Graph& g, double eps) {
     gp_take_kernel<<<blocks_for(nrem, kThreads), kThreads, 0, g.stream>>>(
         P.keys2, nrem, uint32_t(take), idmask, placed, P.batch, P.rem2, P.alive, g.rank.p);
     KCG_LAUNCHED(g);
-    decrement_kernel<<<blocks_for(take * 32, kThreads), kThreads, 0, g.stream>>>(
-        P.batch, uint32_t(take), g.und_off.p, g.und_adj.p, P.alive, P.wdeg);
-    KCG_LAUNCHED(g);
+    decrement(g, P, uint32_t(take));
     std::swap(P.rem, P.rem2);
     nrem -= uint32_t(take);
     placed += uint32_t(take);
@@ -549,8 +612,13 @@ uint64_t estimate_impl(Graph& g, double eps) {
         flag, P.rem, nrem, P.pos, P.batch, P.rem2, P.alive, 2, nullptr, 0);
     KCG_LAUNCHED(g);
     KCG_CUDA(cudaMemsetAsync(P.ctr, 0, 8, g.stream));
+    unsigned* nh = reinterpret_cast<unsigned*>(P.ctr + 4);
+    KCG_CUDA(cudaMemsetAsync(nh, 0, 4, g.stream));
     arb_decrement_kernel<<<blocks_for(uint64_t(nb) * 32, kThreads), kThreads, 0, g.stream>>>(
-        P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, P.ctr);
+        P.batch, nb, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, P.ctr, P.hubs, nh);
+    KCG_LAUNCHED(g);
+    decrement_hub_kernel<true><<<148 * 4, kThreads, 0, g.stream>>>(
+        P.hubs, nh, g.und_off.p, g.und_adj.p, P.alive, P.wdeg, P.ctr);
     KCG_LAUNCHED(g);
     kill_kernel<<<blocks_for(nb, kThreads), kThreads, 0, g.stream>>>(P.batch, nb, P.alive);
     KCG_LAUNCHED(g);
