@@ -810,7 +810,82 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     }
     __syncthreads();
     ull warp_src = 0;
-    if (R == 2) {
+    if (R == 2 && !PV) {
+      // k = 4, counts only: the source's count is the number of triangles
+      // of its induced DAG, sum over induced edges (i, x) of
+      // |N+(i) ∩ N+(x)|.  Rows hold only bits above their own index, so
+      // the sum runs over whole 16-byte groups from x's group on with no
+      // masking.  The edges are split evenly over the threads (row edge
+      // counts -> block scan -> each thread a contiguous edge range), so a
+      // dense row no longer holds its warp.
+      uint32_t* rc = rP;  // free after staging: row edge-count prefix
+      const uint32_t ipt = (d + NT - 1) / NT;
+      const uint32_t r0 = threadIdx.x * ipt, r1 = min(d, r0 + ipt);
+      ull mine = 0;
+      for (uint32_t r = r0; r < r1; r++) {
+        const uint32_t* rr = sym + size_t(r) * wp;
+        uint32_t c = 0;
+        for (uint32_t w = r >> 5; w < W; w++) c += __popc(rr[w]);
+        rc[r] = c;
+        mine += c;
+      }
+      ull excl, E;
+      BlockScanU64(s_scan).ExclusiveSum(mine, excl, E);
+      {
+        uint32_t run = uint32_t(excl);
+        for (uint32_t r = r0; r < r1; r++) {
+          const uint32_t c = rc[r];
+          rc[r] = run;
+          run += c;
+        }
+      }
+      __syncthreads();
+      const uint32_t e0 = uint32_t(E * threadIdx.x / NT), e1 = uint32_t(E * (threadIdx.x + 1) / NT);
+      ull acc = 0;
+      if (e0 < e1) {
+        // row of edge e0: last r with rc[r] <= e0 (rows may be empty)
+        uint32_t lo = 0, hi = d;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (rc[mid] <= e0)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        uint32_t i = lo, skip = e0 - rc[lo];
+        const uint32_t* ri = sym + size_t(i) * wp;
+        uint32_t w = i >> 5, cur = ri[w];
+        const uint32_t G = (W + 3) >> 2;
+        for (uint32_t e = e0; e < e1; e++) {
+          // next set bit in row order (skipping `skip` bits first)
+          for (;;) {
+            while (cur == 0) {
+              if (++w >= W) {
+                ++i;
+                ri = sym + size_t(i) * wp;
+                w = i >> 5;
+              }
+              cur = ri[w];
+            }
+            if (skip == 0) break;
+            cur &= cur - 1;
+            skip--;
+          }
+          const uint32_t x = 32 * w + __ffs(cur) - 1;
+          cur &= cur - 1;
+          const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
+          const uint4* rx4 = reinterpret_cast<const uint4*>(sym + size_t(x) * wp);
+          uint32_t cx = 0;
+          for (uint32_t g = w >> 2; g < G; g++) {
+            const uint4 va = ri4[g], vb = rx4[g];
+            cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
+                  __popc(va.w & vb.w);
+          }
+          acc += cx;
+        }
+      }
+      warp_src = warp_sum(acc);
+    } else if (R == 2) {
       // k = 4: the source's count is the number of triangles of its induced
       // DAG, sum over induced edges (i, x) of |N+(i) ∩ N+(x)|.  Every
       // thread takes upper-triangle bitmap words (i, w) and pops its pairs;
