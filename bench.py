@@ -147,15 +147,14 @@ def alg_bytes(n, out_off, out_adj):
     return 16.0 * n + 20.0 * m + 4.0 * float(np.dot(indeg, outdeg))
 
 
-def ncu_traffic(cfg_id, k):
+def ncu_entry(cfg_id, k):
+    """The committed ncu capture of one counting call (profiles/)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
         return None
     try:
-        d = json.load(open(path))
-        ent = d.get(f"config{cfg_id}_k{k}")
-        return ent.get("dram_bytes_per_launch") if ent else None
-    except (ValueError, KeyError):
+        return json.load(open(path)).get(f"config{cfg_id}_k{k}")
+    except ValueError:
         return None
 
 
@@ -308,13 +307,24 @@ def run_kcg(args):
     peak, peak_src = measured_peaks()
     achieved = b_alg / (phase["count_kernel_ms"] / 1e3) / 1e9
     dag_bytes = 8 * (g.n + 1) + 4 * g.m
+    ncu = ncu_entry(args.config, k)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(args.config, k),
+                "frac": achieved / peak,
+                "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
                 "alg_bytes_per_launch": b_alg, "kernel_ms": phase["count_kernel_ms"],
                 "peak_source": peak_src,
                 "note": "achieved = B_alg (SURVEY.md §8(d): 16n+20m+4*sum indeg*outdeg) / "
                         "device time of the counting kernels; the DAG (%.0f MB) %s L2"
                         % (dag_bytes / 1e6, "fits in" if dag_bytes < 126e6 else "exceeds")}
+    if ncu and "sm_throughput_pct_time_weighted" in ncu:
+        # the limiting roof of the L2-resident counting kernels is integer
+        # issue: ncu's SM throughput = achieved fraction of
+        # peak issue, time-weighted over the launches of one count
+        roofline["issue"] = {
+            "frac": ncu["sm_throughput_pct_time_weighted"] / 100.0,
+            "ipc": ncu["ipc_time_weighted"], "peak_ipc": ncu["issue_slot_peak_ipc"],
+            "threads_per_inst": ncu["threads_per_inst_time_weighted"],
+            "source": "profiles/ncu_summary.json: " + ncu["source"]}
 
     # secondary: the config's other k values on the same DAG (counting only)
     secondary = {}
