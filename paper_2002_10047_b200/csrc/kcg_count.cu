@@ -255,6 +255,7 @@ struct Lvl {
 // Byte layout of one CTA's working set (shared memory or a global slice).
 struct Layout {
   uint32_t dmax, wpmax, tbits, fbits, levels;
+  uint32_t lean;  // k = 4 counts: rows padded to 4 words only, warp areas = queues
   size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
   size_t sym_bytes;  // the bitmap; inside `total` unless sym_apart
   // per-warp offsets
@@ -271,11 +272,20 @@ __host__ __device__ inline uint32_t row_stride(uint32_t W) { return 4u * (((W + 
 
 // sym_apart: the bitmap is laid out separately (a per-CTA slice of global
 // memory) and `total` covers the rest, which stays in shared memory.
+// Row stride of a lean (k = 4 counts) layout: 16-byte rows, no bank padding
+// (the flat pair pass reads unrelated rows per lane).
+__host__ __device__ inline uint32_t lean_stride(uint32_t W) { return (W + 3u) & ~3u; }
+
+// lean: k = 4 counts only -- the edge-search areas of the warps are not
+// needed and the rows drop their bank padding, which buys the (256, 512]
+// and (512, 724] bins one more resident CTA per SM.
 __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bool pv, int nw,
-                                              size_t stk_bytes, bool sym_apart = false) {
+                                              size_t stk_bytes, bool sym_apart = false,
+                                              bool lean = false) {
   Layout L;
   L.dmax = dmax;
-  L.wpmax = row_stride((dmax + 31) / 32);
+  L.lean = lean;
+  L.wpmax = lean ? lean_stride((dmax + 31) / 32) : row_stride((dmax + 31) / 32);
   uint32_t tb = 6;
   while ((1u << tb) < 2 * dmax) tb++;
   L.tbits = tb;
@@ -299,6 +309,12 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   at = align_up(at + (pv ? size_t(dmax) * 8 : 0), 16);
   L.warp0 = at;
   size_t w = 0;
+  if (lean) {
+    L.w_cand = L.w_stack = L.w_csym = L.w_cusym = L.w_cpv = L.w_lvl = L.w_stk = L.w_q = 0;
+    L.warp_stride = 128 * 4;
+    L.total = align_up(at + L.warp_stride * nw, 128);
+    return L;
+  }
   L.w_cand = w;
   w = align_up(w + 32 * 4 + 128, 16);
   L.w_stack = w;
@@ -738,7 +754,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     const uint32_t slice = a.item_sl[si] >> 16, nsl = a.item_sl[si] & 0xffffu;
     const uint64_t b = a.off[u];
     const uint32_t d = uint32_t(a.off[u + 1] - b);
-    const uint32_t W = (d + 31) / 32, wp = row_stride(W);
+    const uint32_t W = (d + 31) / 32, wp = L.lean ? lean_stride(W) : row_stride(W);
     uint32_t tb = 6;
     while ((1u << tb) < 2 * d) tb++;
     const uint32_t fb = tb + 4 > 14 ? (tb + 4 > 20 ? 20 : tb + 4) : 14;
@@ -1092,8 +1108,12 @@ void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaS
     launch_cta_t<PV, WS_GLOBAL, 512, MAXL>(g, a, heavy_budget, st);
   else if (gws == WS_SYM_GLOBAL)
     launch_cta_t<PV, WS_SYM_GLOBAL, 512, MAXL>(g, a, heavy_budget, st);
-  else if (nt == 512)
+  else if (nt == 512) {
+    if constexpr (MAXL == 0 && !PV) {  // lean k = 4: two 512-thread CTAs per SM
+      if (a.k == 4) return launch_cta_t<PV, WS_SMEM, 512, MAXL, 2>(g, a, heavy_budget, st);
+    }
     launch_cta_t<PV, WS_SMEM, 512, MAXL>(g, a, heavy_budget, st);
+  }
   else {
     if constexpr (MAXL == 0) {
       if (a.k == 4) return launch_cta_t<PV, WS_SMEM, 256, MAXL, 4>(g, a, heavy_budget, st);
@@ -1293,7 +1313,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
         while (end < nc && deg_at(end) > lo) end++;
         if (end == pos) continue;
         const int nt = hi > 512 ? 512 : 256;
-        Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes);
+        Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes, false, k == 4 && !want_pv);
         if (Lb.total > smem_cap)
           global_plan(pos, end, deg_at(pos));
         else
