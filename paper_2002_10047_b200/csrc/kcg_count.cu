@@ -1114,7 +1114,12 @@ void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaS
     }
     launch_cta_t<PV, WS_SMEM, 512, MAXL>(g, a, heavy_budget, st);
   }
-  else {
+  else if (nt == 128) {
+    if constexpr (MAXL == 0 && !PV) {
+      if (a.k == 4) return launch_cta_t<PV, WS_SMEM, 128, MAXL, 8>(g, a, heavy_budget, st);
+    }
+    fail(KCG_ERUNTIME, "128-thread counting CTAs are only planned for k = 4 counts");
+  } else {
     if constexpr (MAXL == 0) {
       if (a.k == 4) return launch_cta_t<PV, WS_SMEM, 256, MAXL, 4>(g, a, heavy_budget, st);
     }
@@ -1312,8 +1317,11 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
         uint32_t end = pos;
         while (end < nc && deg_at(end) > lo) end++;
         if (end == pos) continue;
-        const int nt = hi > 512 ? 512 : 256;
-        Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes, false, k == 4 && !want_pv);
+        const bool lean = k == 4 && !want_pv;
+        // lean small sources: 128-thread CTAs (per-source barriers and
+        // scans over fewer warps, more sources in flight per SM)
+        const int nt = hi > 512 ? 512 : (lean && hi <= 256) ? 128 : 256;
+        Layout Lb = make_layout(hi, levels, want_pv, nt / 32, sbytes, false, lean);
         if (Lb.total > smem_cap)
           global_plan(pos, end, deg_at(pos));
         else
