@@ -826,22 +826,28 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     }
     __syncthreads();
     ull warp_src = 0;
-    if (R == 2 && !PV) {
-      // k = 4, counts only: the source's count is the number of triangles
-      // of its induced DAG, sum over induced edges (i, x) of
-      // |N+(i) ∩ N+(x)|.  Rows hold only bits above their own index, so
-      // the sum runs over whole 16-byte groups from x's group on with no
-      // masking.  The edges are split evenly over the threads (row edge
-      // counts -> block scan -> each thread a contiguous edge range), so a
-      // dense row no longer holds its warp.
+    if (R == 2) {
+      // k = 4: the source's count is the number of triangles of its induced
+      // DAG, sum over induced edges (i, x) of |N+(i) ∩ N+(x)|.  The edges
+      // are split evenly over the threads (row edge counts -> block scan ->
+      // each thread a contiguous edge range), so a dense row no longer
+      // holds its warp.  Counts only: rows hold only bits above their own
+      // index and the sum runs over whole 16-byte groups from x's group on.
+      // Per-vertex: rows are symmetric; x is credited with its 3rd-vertex
+      // cliques (cx) and its top-vertex cliques with (i, y), i < y < x
+      // (`lower`), i with its 2nd-vertex cliques (flushed per row).
       uint32_t* rc = rP;  // free after staging: row edge-count prefix
       const uint32_t ipt = (d + NT - 1) / NT;
       const uint32_t r0 = threadIdx.x * ipt, r1 = min(d, r0 + ipt);
+      auto up_word = [&](const uint32_t* rr, uint32_t r, uint32_t w) -> uint32_t {
+        const uint32_t v = rr[w];
+        return (PV && w == (r >> 5)) ? v & above_mask(r & 31) : v;
+      };
       ull mine = 0;
       for (uint32_t r = r0; r < r1; r++) {
         const uint32_t* rr = sym + size_t(r) * wp;
         uint32_t c = 0;
-        for (uint32_t w = r >> 5; w < W; w++) c += __popc(rr[w]);
+        for (uint32_t w = r >> 5; w < W; w++) c += __popc(up_word(rr, r, w));
         rc[r] = c;
         mine += c;
       }
@@ -870,18 +876,25 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
         }
         uint32_t i = lo, skip = e0 - rc[lo];
         const uint32_t* ri = sym + size_t(i) * wp;
-        uint32_t w = i >> 5, cur = ri[w];
+        uint32_t w = i >> 5, cur = up_word(ri, i, w);
         const uint32_t G = (W + 3) >> 2;
+        ull ci = 0;  // PV: row i's 2nd-vertex credit
         for (uint32_t e = e0; e < e1; e++) {
           // next set bit in row order (skipping `skip` bits first)
           for (;;) {
             while (cur == 0) {
               if (++w >= W) {
+                if constexpr (PV) {
+                  if (ci) atomicAdd(&pvl[i], ci);
+                  ci = 0;
+                }
                 ++i;
                 ri = sym + size_t(i) * wp;
                 w = i >> 5;
+                cur = up_word(ri, i, w);
+              } else {
+                cur = ri[w];
               }
-              cur = ri[w];
             }
             if (skip == 0) break;
             cur &= cur - 1;
@@ -890,67 +903,48 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
           const uint32_t x = 32 * w + __ffs(cur) - 1;
           cur &= cur - 1;
           const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
-          const uint4* rx4 = reinterpret_cast<const uint4*>(sym + size_t(x) * wp);
+          const uint32_t* rx = sym + size_t(x) * wp;
+          const uint4* rx4 = reinterpret_cast<const uint4*>(rx);
           uint32_t cx = 0;
-          for (uint32_t g = w >> 2; g < G; g++) {
-            const uint4 va = ri4[g], vb = rx4[g];
-            cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
-                  __popc(va.w & vb.w);
+          if constexpr (PV) {
+            // one pass from i's group: all = |N+(i) ∩ N(x)| (x as 3rd or as
+            // top vertex: bit x of row x is clear, so this is exactly
+            // cx + #{y : i < y < x}), cx = the part above x
+            const uint32_t wi = i >> 5, gx = w >> 2;
+            uint32_t all = 0;
+            for (uint32_t g = wi >> 2; g < G; g++) {
+              const uint4 va = ri4[g], vb = rx4[g];
+              uint32_t m[4] = {va.x & vb.x, va.y & vb.y, va.z & vb.z, va.w & vb.w};
+              if (g == (wi >> 2)) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                  const uint32_t wd = 4 * g + j;
+                  m[j] &= wd < wi ? 0u : wd == wi ? above_mask(i & 31) : FULL;
+                }
+              }
+              all += __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+              if (g >= gx) {
+                if (g == gx) {
+#pragma unroll
+                  for (int j = 0; j < 4; j++) {
+                    const uint32_t wd = 4 * g + j;
+                    m[j] &= wd < w ? 0u : wd == w ? above_mask(x & 31) : FULL;
+                  }
+                }
+                cx += __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+              }
+            }
+            ci += cx;
+            if (all) atomicAdd(&pvl[x], ull(all));
+          } else {
+            for (uint32_t g = w >> 2; g < G; g++) {
+              const uint4 va = ri4[g], vb = rx4[g];
+              cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
+                    __popc(va.w & vb.w);
+            }
           }
           acc += cx;
         }
-      }
-      warp_src = warp_sum(acc);
-    } else if (R == 2) {
-      // k = 4: the source's count is the number of triangles of its induced
-      // DAG, sum over induced edges (i, x) of |N+(i) ∩ N+(x)|.  Every
-      // thread takes upper-triangle bitmap words (i, w) and pops its pairs;
-      // no per-edge scheduling or member gather.
-      ull acc = 0;
-      for (uint32_t q = threadIdx.x; q < d * W; q += NT) {
-        const uint32_t i = q / W, w = q - i * W;
-        if (w < (i >> 5)) continue;
-        const uint32_t* ri = sym + size_t(i) * wp;
-        uint32_t bits = ri[w];
-        if (w == (i >> 5)) bits &= above_mask(i & 31);
-        if (!bits) continue;
-        // row i's words after w in w's 16-byte group, masked once; word w
-        // itself is `bits`, which after popping x is exactly row_i[w] above x
-        const uint4* ri4 = reinterpret_cast<const uint4*>(ri);
-        const uint32_t g0 = w >> 2, G = (W + 3) >> 2, wj = w & 3;
-        uint4 vp = ri4[g0];
-        vp.x = 0;
-        if (wj >= 1) vp.y = 0;
-        if (wj >= 2) vp.z = 0;
-        if (wj >= 3) vp.w = 0;
-        ull ci = 0;
-        while (bits) {
-          const uint32_t x = 32 * w + __ffs(bits) - 1;
-          bits &= bits - 1;
-          const uint32_t* rx = sym + size_t(x) * wp;
-          // |row_i ∩ row_x| above x, 4 words per 128-bit load
-          const uint4* rx4 = reinterpret_cast<const uint4*>(rx);
-          uint4 vb = rx4[g0];
-          uint32_t cx = __popc(bits & rx[w]) + __popc(vp.y & vb.y) + __popc(vp.z & vb.z) +
-                        __popc(vp.w & vb.w);
-          for (uint32_t g = g0 + 1; g < G; g++) {
-            const uint4 va = ri4[g];
-            vb = rx4[g];
-            cx += __popc(va.x & vb.x) + __popc(va.y & vb.y) + __popc(va.z & vb.z) +
-                  __popc(va.w & vb.w);
-          }
-          ci += cx;
-          if constexpr (PV) {
-            // x's degree inside N+(u) ∩ N+(i): also counts the 4th-vertex role
-            const uint32_t wi = i >> 5;
-            uint32_t all = cx + __popc(ri[w] & rx[w] & ~above_mask(x & 31) &
-                                       (w == wi ? above_mask(i & 31) : FULL));
-            for (uint32_t w2 = wi; w2 < w; w2++)
-              all += __popc(ri[w2] & rx[w2] & (w2 == wi ? above_mask(i & 31) : FULL));
-            if (all) atomicAdd(&pvl[x], ull(all));
-          }
-        }
-        acc += ci;
         if constexpr (PV) {
           if (ci) atomicAdd(&pvl[i], ci);
         }
