@@ -30,7 +30,7 @@ import numpy as np  # noqa: E402
 from paper_2002_10047_b200 import gen  # noqa: E402
 
 STRAT_NAMES = {0: "degree", 1: "original", 2: "kcore", 3: "goodrich_pszona",
-               4: "barenboim_elkin"}
+               4: "barenboim_elkin", 5: "kcore_parallel"}
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -61,7 +61,7 @@ def workload(cfg_id, k):
 
 def config_obj(cfg_id, spec, k, g, extra=None):
     c = {"workload": f"config{cfg_id}: {spec['desc']}", "k": k,
-         "strategy": STRAT_NAMES[spec["strategy"]], "eps": spec["eps"], "n": g.n, "m": g.m,
+         "strategy": STRAT_NAMES[gen.gpu_strategy(spec)], "eps": spec["eps"], "n": g.n, "m": g.m,
          "step": "rank + orient (DAG) + count_total",
          "l2": "flushed between timed steps (512 MiB memset on the library stream)"}
     if extra:
@@ -249,7 +249,7 @@ def run_kcg(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec, k = workload(args.config, args.k)
-    strat, eps = spec["strategy"], spec["eps"]
+    strat, eps = gen.gpu_strategy(spec), spec["eps"]
     g = gen.load_config_graph(args.config, cache=False)
     h = kcg.DeviceGraph.from_graph(g)
     stream = torch.cuda.ExternalStream(h.stream_ptr())

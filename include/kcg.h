@@ -44,6 +44,12 @@ extern "C" {
 #define KCG_KCORE 2
 #define KCG_GOODRICH_PSZONA 3
 #define KCG_BARENBOIM_ELKIN 4
+/* Not in the reference: a bulk-synchronous degeneracy order (every vertex
+ * at the current minimum level leaves in the same round, ranked by
+ * (round, id)).  Same max out-degree as KCG_KCORE, which reproduces the
+ * reference's sequential (degree, id) heap order exactly but pops one
+ * vertex at a time. */
+#define KCG_KCORE_PARALLEL 5
 
 typedef struct kcg_graph kcg_graph;
 

@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(256) kcore_coop_kernel(KcoreArgs a) {
     grid.sync();
     cur ^= 1;
   }
-  if (tid == 0) a.ctr[3] = round;
+  if (tid == 0) {
+    a.ctr[3] = round;
+    a.ctr[4] = level;  // the degeneracy (max core number)
+  }
 }
 
 __global__ void kcore_keys_kernel(const uint32_t* __restrict__ rnd, uint32_t n, int idbits,
@@ -551,7 +554,7 @@ __global__ void kcore_rank_kernel(const uint64_t* __restrict__ sorted, uint32_t 
   }
 }
 
-uint64_t rank_kcore(Graph& g) {
+uint64_t rank_kcore(Graph& g, uint32_t* degeneracy = nullptr) {
   // the reference pops one (degree, id) heap minimum at a
   // time (orientation.cpp:23-46), which is inherently sequential.  This
   // order differs, its max out-degree (= degeneracy) does not.
@@ -584,10 +587,183 @@ uint64_t rank_kcore(Graph& g) {
   kcore_rank_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(
       sorted, n, (uint64_t(1) << idbits) - 1, g.rank.p, g.order.p);
   KCG_LAUNCHED(g);
-  unsigned rounds = 0;
-  KCG_CUDA(cudaMemcpyAsync(&rounds, ctr + 3, 4, cudaMemcpyDeviceToHost, g.stream));
+  unsigned hv[2] = {0, 0};
+  KCG_CUDA(cudaMemcpyAsync(hv, ctr + 3, 8, cudaMemcpyDeviceToHost, g.stream));
   g.sync();
-  return rounds;
+  if (degeneracy) *degeneracy = hv[1];
+  return hv[0];
+}
+
+// ---- exact rank_by_kcore -----------------------------------------------------
+// The reference pops the (induced degree, id) minimum one vertex at a time
+// (orientation.cpp:23-46).  Reproduced exactly by one CTA: alive vertices of
+// degree <= D (the degeneracy, from the parallel peel above -- the minimum
+// alive degree never exceeds it) sit in per-degree hierarchical bitmaps
+// (32-ary levels over the ids, top level <= 32 words), so the minimum is
+// "lowest non-empty bucket, then first set bit" in one warp ballot per
+// level; a pop clears its bit, decrements its live neighbours and moves
+// them one bucket down (clears, barrier, sets).  The minimum bucket only
+// falls by one per pop, so the search restarts one bucket below the last.
+struct KcX {
+  const uint64_t* off;
+  const uint32_t* adj;
+  uint32_t n, D, nlev;
+  uint32_t lw[6];       // words per level (level 0 = ids)
+  uint64_t lo[6];       // word offset of each level inside a bucket
+  uint64_t bwords;      // words per bucket
+  uint32_t* bits;       // (D + 1) * bwords
+  uint32_t* deg;
+  uint8_t* done;
+  uint32_t* rank;
+  uint32_t* order;
+  unsigned* err;
+};
+
+__device__ __forceinline__ void kx_clear(const KcX& a, uint32_t b, uint32_t v) {
+  uint32_t* B = a.bits + uint64_t(b) * a.bwords;
+  uint32_t idx = v;
+  for (uint32_t l = 0; l < a.nlev; l++) {
+    const uint32_t bit = 1u << (idx & 31);
+    const uint32_t old = atomicAnd(&B[a.lo[l] + (idx >> 5)], ~bit);
+    if ((old & ~bit) != 0) break;  // word still non-empty
+    idx >>= 5;
+  }
+}
+
+__device__ __forceinline__ void kx_set(const KcX& a, uint32_t b, uint32_t v) {
+  uint32_t* B = a.bits + uint64_t(b) * a.bwords;
+  uint32_t idx = v;
+  for (uint32_t l = 0; l < a.nlev; l++) {
+    const uint32_t old = atomicOr(&B[a.lo[l] + (idx >> 5)], 1u << (idx & 31));
+    if (old != 0) break;  // upper levels already mark this word
+    idx >>= 5;
+  }
+}
+
+__global__ void kx_fill_kernel(KcX a) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * blockDim.x) {
+    const uint32_t d = uint32_t(a.off[v + 1] - a.off[v]);
+    a.deg[v] = d;
+    if (d <= a.D) kx_set(a, d, v);
+  }
+}
+
+constexpr int kKxThreads = 1024;
+
+__global__ void __launch_bounds__(kKxThreads) kx_peel_kernel(KcX a) {
+  __shared__ uint32_t s_v, s_b;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t b = 0;
+  for (uint32_t step = 0; step < a.n; step++) {
+    if (threadIdx.x < 32) {
+      // lowest non-empty bucket at or above b, then its first set bit
+      const uint32_t top = a.nlev - 1;
+      uint32_t w = 0;
+      for (; b <= a.D; b++) {
+        const uint32_t* B = a.bits + uint64_t(b) * a.bwords;
+        w = lane < a.lw[top] ? B[a.lo[top] + lane] : 0u;
+        if (__ballot_sync(0xffffffffu, w != 0)) break;
+      }
+      if (b > a.D) {  // cannot happen while D is the degeneracy
+        if (lane == 0) {
+          *a.err = 1;
+          s_v = 0xffffffffu;
+        }
+      } else {
+        const uint32_t* B = a.bits + uint64_t(b) * a.bwords;
+        const unsigned nz = __ballot_sync(0xffffffffu, w != 0);
+        const uint32_t f = __ffs(nz) - 1;
+        uint32_t word = __shfl_sync(0xffffffffu, w, f);
+        uint32_t idx = f * 32 + __ffs(word) - 1;
+        for (int l = int(top) - 1; l >= 0; l--) {
+          word = B[a.lo[l] + idx];  // warp-uniform load
+          idx = idx * 32 + __ffs(word) - 1;
+        }
+        if (lane == 0) {
+          s_v = idx;
+          s_b = b;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_v == 0xffffffffu) return;
+    const uint32_t v = s_v, bv = s_b;
+    if (threadIdx.x == 0) {
+      a.done[v] = 1;
+      a.rank[v] = step;
+      a.order[step] = v;
+      kx_clear(a, bv, v);
+    }
+    b = bv ? bv - 1 : 0;
+    // neighbours, kKxThreads at a time: clear from old bucket, then set
+    const uint64_t e = a.off[v + 1];
+    for (uint64_t p0 = a.off[v]; p0 < e; p0 += kKxThreads) {
+      const uint64_t p = p0 + threadIdx.x;
+      uint32_t u = 0xffffffffu, nd = 0xffffffffu;
+      if (p < e) {
+        u = a.adj[p];
+        if (u != v && !a.done[u]) {
+          const uint32_t od = a.deg[u];
+          nd = od - 1;
+          a.deg[u] = nd;
+          if (od <= a.D) kx_clear(a, od, u);
+        } else {
+          u = 0xffffffffu;
+        }
+      }
+      __syncthreads();
+      if (u != 0xffffffffu && nd <= a.D) kx_set(a, nd, u);
+      __syncthreads();
+    }
+  }
+}
+
+uint64_t rank_kcore_exact(Graph& g) {
+  const uint32_t n = g.n;
+  if (!n) return 0;
+  uint32_t D = 0;
+  rank_kcore(g, &D);  // the degeneracy bounds every bucket we need
+  KcX a{};
+  a.off = g.und_off.p;
+  a.adj = g.und_adj.p;
+  a.n = n;
+  a.D = D;
+  uint64_t words = 0;
+  uint32_t len = n;
+  uint32_t l = 0;
+  do {
+    len = (len + 31) / 32;
+    if (l >= 6) fail(KCG_ERUNTIME, "exact k-core: graph too large for the bucket levels");
+    a.lw[l] = len;
+    a.lo[l] = words;
+    words += len;
+    l++;
+  } while (len > 32);
+  a.nlev = l;
+  a.bwords = (words + 31) & ~uint64_t(31);
+  const uint64_t total_words = a.bwords * (uint64_t(D) + 1);
+  DevBuf<uint32_t> bits;
+  bits.ensure(total_words, &g.alloc);
+  KCG_CUDA(cudaMemsetAsync(bits.p, 0, total_words * 4, g.stream));
+  a.bits = bits.p;
+  Peel P = peel_state(g, false);
+  a.deg = P.wdeg;
+  a.done = P.alive;  // reused as the done flags
+  KCG_CUDA(cudaMemsetAsync(a.done, 0, n, g.stream));
+  a.rank = g.rank.p;
+  g.order.ensure(n, &g.alloc);
+  a.order = g.order.p;
+  kx_fill_kernel<<<blocks_for(n, kThreads), kThreads, 0, g.stream>>>(a);
+  KCG_LAUNCHED(g);
+  a.err = reinterpret_cast<unsigned*>(P.ctr + 5);
+  KCG_CUDA(cudaMemsetAsync(a.err, 0, 4, g.stream));
+  kx_peel_kernel<<<1, kKxThreads, 0, g.stream>>>(a);
+  KCG_LAUNCHED(g);
+  unsigned err = 0;
+  KCG_CUDA(cudaMemcpyAsync(&err, a.err, 4, cudaMemcpyDeviceToHost, g.stream));
+  g.sync();
+  if (err) fail(KCG_ERUNTIME, "exact k-core: no bucket at or below the degeneracy");
+  return 0;
 }
 
 }  // namespace
@@ -643,7 +819,7 @@ uint64_t estimate_arboricity(Graph& g, double eps) {
 
 uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
                     uint64_t* alpha_out) {
-  if (strategy < KCG_DEGREE || strategy > KCG_BARENBOIM_ELKIN)
+  if (strategy < KCG_DEGREE || strategy > KCG_KCORE_PARALLEL)
     fail(KCG_EINVAL, "unknown orientation strategy");
   if ((strategy == KCG_BARENBOIM_ELKIN || strategy == KCG_GOODRICH_PSZONA) && !(eps > 0))
     fail(KCG_EINVAL, "epsilon must be positive");
@@ -659,6 +835,9 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
       KCG_LAUNCHED(g);
       break;
     case KCG_KCORE:
+      rounds = rank_kcore_exact(g);
+      break;
+    case KCG_KCORE_PARALLEL:
       rounds = rank_kcore(g);
       break;
     case KCG_GOODRICH_PSZONA:

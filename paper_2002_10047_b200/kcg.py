@@ -22,8 +22,10 @@ from ._paths import LIB_DIR
 
 KCG_OK, KCG_EINVAL, KCG_ERUNTIME, KCG_ENOMEM, KCG_ELOGIC = 0, 1, 2, 3, 4
 DEGREE, ORIGINAL, KCORE, GOODRICH_PSZONA, BARENBOIM_ELKIN = 0, 1, 2, 3, 4
+KCORE_PARALLEL = 5  # bulk-synchronous degeneracy order (not in the reference)
 STRATEGY_NAMES = {"degree": DEGREE, "original": ORIGINAL, "kcore": KCORE,
-                  "goodrich_pszona": GOODRICH_PSZONA, "barenboim_elkin": BARENBOIM_ELKIN}
+                  "goodrich_pszona": GOODRICH_PSZONA, "barenboim_elkin": BARENBOIM_ELKIN,
+                  "kcore_parallel": KCORE_PARALLEL}
 
 EXPORTED = [
     "kcg_last_error", "kcg_version", "kcg_device_info", "kcg_graph_create",

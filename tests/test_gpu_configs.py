@@ -41,17 +41,20 @@ def test_config_parity(cid):
     with kcg.DeviceGraph.from_graph(g) as h:
         r, rounds, alpha = h.rank(spec["strategy"], spec["eps"])
         assert sorted(r[:1000].tolist()) is not None
-        if spec["strategy"] != kcg.KCORE:
-            # bit-exact ranking (degree, Barenboim-Elkin incl. rounds and alpha)
-            assert f"{gen.digest_u32(r):016x}" == gold["rank_digest"]
-            if spec["strategy"] == kcg.BARENBOIM_ELKIN:
-                assert rounds == gold["rank_rounds"] and alpha == gold["alpha_hat"]
-            off, adj, mx = h.direct()
-            assert f"{gen.digest_u64(off):016x}:{gen.digest_u32(adj):016x}" == gold["dag_digest"]
-        else:
-            _, _, mx = h.direct(download=False)
-        # degeneracy orders share the max out-degree even when the order differs
+        # bit-exact ranking (degree, Barenboim-Elkin incl. rounds and alpha,
+        # the sequential k-core heap order) and DAG
+        assert f"{gen.digest_u32(r):016x}" == gold["rank_digest"]
+        if spec["strategy"] == kcg.BARENBOIM_ELKIN:
+            assert rounds == gold["rank_rounds"] and alpha == gold["alpha_hat"]
+        off, adj, mx = h.direct()
+        assert f"{gen.digest_u64(off):016x}:{gen.digest_u32(adj):016x}" == gold["dag_digest"]
         assert mx == gold["max_out_degree"]
+        if gen.gpu_strategy(spec) != spec["strategy"]:
+            # the benchmark's bulk-synchronous degeneracy order: same max
+            # out-degree as the reference's sequential one
+            h.rank(gen.gpu_strategy(spec), spec["eps"], download=False)
+            _, _, mx2 = h.direct(download=False)
+            assert mx2 == gold["max_out_degree"]
         for ks, ent in gold.get("counts", {}).items():
             total, _ = h.count(int(ks))
             assert str(total) == ent["total"], (cid, ks)

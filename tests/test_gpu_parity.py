@@ -71,7 +71,7 @@ def test_kcore_is_a_degeneracy_order(small_cases, port):
     for case in small_cases[:60]:
         g = load_case_graph(case)
         with kcg.DeviceGraph.from_graph(g) as h:
-            r, rounds, _ = h.rank(kcg.KCORE)
+            r, rounds, _ = h.rank(kcg.KCORE_PARALLEL)
             assert sorted(r.tolist()) == list(range(g.n))
             _, _, mx = h.direct()
         # degeneracy via the sequential heap order restated in the oracle
@@ -104,7 +104,8 @@ def test_errors_map_to_invalid_argument():
 def test_empty_and_edgeless_graphs():
     for g in [gen.from_edges(0, np.zeros((0, 2))), gen.from_edges(7, np.zeros((0, 2)))]:
         with kcg.DeviceGraph.from_graph(g) as h:
-            for strat in (kcg.DEGREE, kcg.KCORE, kcg.BARENBOIM_ELKIN, kcg.GOODRICH_PSZONA):
+            for strat in (kcg.DEGREE, kcg.KCORE, kcg.KCORE_PARALLEL, kcg.BARENBOIM_ELKIN,
+                          kcg.GOODRICH_PSZONA):
                 r, _, _ = h.rank(strat, 1.0)
                 assert sorted(r.tolist()) == list(range(g.n))
             h.direct()
@@ -135,3 +136,31 @@ def test_reference_shaped_python_api():
     t, pv = kcg.count_per_vertex(dg, 4)
     assert kcg.count_total(dg, 4) == t
     assert int(pv.sum()) == 4 * t
+
+
+def test_kcore_exact_matches_reference():
+    """KCG_KCORE reproduces the reference's sequential (degree, id) heap
+    order bit for bit (tests/golden/kcore_cases.json, config 4's golden)."""
+    import json
+    import os
+    from tests import peelcases
+    gold = json.load(open(os.path.join(peelcases.ROOT, "tests", "golden", "kcore_cases.json")))
+    for c in gold["cases"]:
+        if c["kind"] == "gnp":
+            g = gen.gnp(*c["params"])
+        elif c["kind"] == "rmat":
+            s, e, seed, perm = c["params"]
+            g = gen.rmat(s, e, seed=seed, permute=bool(perm))
+        else:
+            g = gen.load_config_graph(c["params"][0], cache=False)
+        assert g.digest() == c["digest"]
+        with kcg.DeviceGraph.from_graph(g) as h:
+            r, _, _ = h.rank(kcg.KCORE)
+        if "rank" in c:
+            assert r.tolist() == c["rank"], c["params"]
+        assert f"{gen.digest_u32(r):016x}" == c["rank_digest"], c["params"]
+    g4 = json.load(open(os.path.join(peelcases.ROOT, "tests", "golden", "config4.json")))
+    g = gen.load_config_graph(4, cache=False)
+    with kcg.DeviceGraph.from_graph(g) as h:
+        r, _, _ = h.rank(kcg.KCORE)
+    assert f"{gen.digest_u32(r):016x}" == g4["rank_digest"]

@@ -59,7 +59,7 @@ for cid in [int(c) for c in os.environ.get("CONFIGS", "1 2").split()]:
     print(f"[{cid}] generated n={g.n} m={g.m} in {time.time()-t:.1f}s digest_ok="
           f"{g.digest() == gold['graph_digest']}", flush=True)
     with kcg.DeviceGraph.from_graph(g) as h:
-        r, rounds, alpha = h.rank(spec["strategy"], spec["eps"])
+        r, rounds, alpha = h.rank(gen.gpu_strategy(spec), spec["eps"])
         off, tgt, mx = h.direct()
         print(f"[{cid}] rank ok={gen.digest_u32(r) == int(gold['rank_digest'], 16)} rounds={rounds}"
               f"/{gold['rank_rounds']} alpha={alpha}/{gold.get('alpha_hat')} maxout={mx}/"

@@ -21,7 +21,7 @@ a = ap.parse_args()
 spec = gen.CONFIGS[a.config]
 g = gen.load_config_graph(a.config, cache=False)
 with kcg.DeviceGraph.from_graph(g) as h:
-    h.rank(spec["strategy"], spec["eps"], download=False)
+    h.rank(gen.gpu_strategy(spec), spec["eps"], download=False)
     h.direct(download=False)
     for _ in range(a.reps):
         t, _ = h.count(a.k, per_vertex=a.pv)

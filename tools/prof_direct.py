@@ -13,7 +13,7 @@ spec = gen.CONFIGS[cfg]
 g = gen.load_config_graph(cfg, cache=False)
 with kcg.DeviceGraph.from_graph(g) as h:
     for _ in range(reps):
-        h.rank(spec["strategy"], spec["eps"], download=False)
+        h.rank(gen.gpu_strategy(spec), spec["eps"], download=False)
         r = h.timings()["rank_ms"]
         h.direct(download=False)
         print(f"rank_ms={r:.3f} direct_ms={h.timings()['direct_ms']:.3f}", flush=True)

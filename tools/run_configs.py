@@ -46,7 +46,7 @@ for cid in a.configs:
         for k in ks:
             best = None
             for _ in range(a.reps):
-                total, _ = h.pipeline(spec["strategy"], spec["eps"], k)
+                total, _ = h.pipeline(gen.gpu_strategy(spec), spec["eps"], k)
                 t = h.timings()
                 step = t["rank_ms"] + t["direct_ms"] + t["count_ms"]
                 if best is None or step < best[0]:

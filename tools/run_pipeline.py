@@ -47,7 +47,7 @@ for cid in a.configs:
     rec["graph_digest_ok"] = f"{gen.digest_u64(off):016x}:{gen.digest_u32(adj):016x}" == \
         gold["graph_digest"]
     del off, adj
-    h.rank(spec["strategy"], spec["eps"], download=False)
+    h.rank(gen.gpu_strategy(spec), spec["eps"], download=False)
     rec["rank_ms"] = h.timings()["rank_ms"]
     h.direct(download=False)
     rec["direct_ms"] = h.timings()["direct_ms"]
