@@ -43,8 +43,6 @@ typedef unsigned long long ull;
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t NOTFOUND = 0xffffffffu;
-constexpr int CTA_THREADS = 256;
-constexpr int CTA_WARPS = CTA_THREADS / 32;
 constexpr int WARP_THREADS_BLOCK = 256;
 constexpr int WARP_TIER_WARPS = WARP_THREADS_BLOCK / 32;
 constexpr uint32_t SMEM_TIER_MAX = 1024;  // largest d staged in shared memory

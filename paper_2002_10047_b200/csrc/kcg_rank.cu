@@ -183,70 +183,6 @@ __global__ void kill_kernel(const uint32_t* __restrict__ batch, uint32_t nb,
     alive[batch[i]] = 0;
 }
 
-// k-core round: frontier vertices are already dead; a survivor whose
-// degree crosses level+1 -> level joins the next frontier exactly once.
-__global__ void kcore_decrement_kernel(const uint32_t* __restrict__ front, uint32_t nf,
-                                       const uint64_t* __restrict__ off,
-                                       const uint32_t* __restrict__ adj,
-                                       const uint8_t* __restrict__ alive,
-                                       uint32_t* __restrict__ deg, uint32_t level,
-                                       uint32_t* __restrict__ next,
-                                       unsigned long long* __restrict__ nnext) {
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nf;
-       w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    uint32_t v = front[w];
-    for (uint64_t p0 = off[v]; p0 < off[v + 1]; p0 += 32) {
-      uint64_t p = p0 + lane;
-      bool join = false;
-      uint32_t u = 0;
-      if (p < off[v + 1]) {
-        u = adj[p];
-        if (alive[u]) join = atomicSub(&deg[u], 1u) == level + 1;
-      }
-      // warp-aggregated append to the next frontier
-      unsigned ball = __ballot_sync(0xffffffffu, join);
-      if (ball) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(nnext, (unsigned long long)__popc(ball));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (join) next[base + __popc(ball & ((1u << lane) - 1))] = u;
-      }
-    }
-  }
-}
-
-__global__ void kcore_kill_rank_kernel(const uint32_t* __restrict__ front, uint32_t nf,
-                                       uint32_t placed, uint8_t* __restrict__ alive,
-                                       uint32_t* __restrict__ rank) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
-    uint32_t v = front[i];
-    alive[v] = 0;
-    rank[v] = placed + i;
-  }
-}
-
-struct AliveDeg {  // min-degree reduction over alive remaining vertices
-  const uint32_t* rem;
-  const uint32_t* deg;
-  const uint8_t* alive;
-  __device__ uint32_t operator()(uint32_t i) const {
-    uint32_t v = rem[i];
-    return alive[v] ? deg[v] : 0xffffffffu;
-  }
-};
-struct AliveSel {
-  const uint8_t* alive;
-  __device__ bool operator()(uint32_t v) const { return alive[v] != 0; }
-};
-struct AtLevel {
-  const uint32_t* rem;
-  const uint32_t* deg;
-  const uint8_t* alive;
-  uint32_t level;
-  __device__ bool operator()(uint32_t v) const { return alive[v] && deg[v] <= level; }
-};
-
 __global__ void gp_keys_kernel(const uint32_t* __restrict__ rem, uint32_t nrem,
                                const uint32_t* __restrict__ deg, int idbits,
                                uint64_t* __restrict__ keys) {
