@@ -43,6 +43,8 @@ def parse_args():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the per-config sweep reported under `configs`")
     ap.add_argument("--cpu-budget-s", type=float, default=240.0,
                     help="wall budget for the reference arm's timed steps")
     return ap.parse_args()
@@ -238,6 +240,47 @@ def cpu_baseline(g, spec, k):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def config_sweep(kcg, skip_cfg):
+    """One line per (config, k[, per-vertex]) with the reference goldens'
+    verdict (tests/golden/config*.json)."""
+    out = []
+    for cid in (1, 2, 3, 4, 5):
+        spec = gen.CONFIGS[cid]
+        strat = gen.gpu_strategy(spec)
+        gpath = os.path.join(ROOT, "tests", "golden", f"config{cid}.json")
+        golden = json.load(open(gpath)) if os.path.exists(gpath) else {}
+        t0 = time.perf_counter()
+        if cid == 5:
+            p = spec["rmat"]
+            h = kcg.DeviceGraph.rmat(p["scale"], p["samples"], seed=p["seed"],
+                                     permute=p["permute"])
+        else:
+            h = kcg.DeviceGraph.from_graph(gen.load_config_graph(cid, cache=False))
+        build_s = time.perf_counter() - t0
+        h.rank(strat, spec["eps"], download=False)
+        rank_ms = h.timings()["rank_ms"]
+        h.direct(download=False)
+        direct_ms = h.timings()["direct_ms"]
+        m = h.m
+        for k in spec["ks"]:
+            for pv in ([False, True] if k in spec["pv_ks"] else [False]):
+                if cid != 5:
+                    h.count(k, per_vertex=pv)  # warm
+                total, _ = h.count(k, per_vertex=pv)
+                cms = h.timings()["count_ms"]
+                step = rank_ms + direct_ms + cms
+                gold = golden.get("counts", {}).get(str(k), {}).get("total")
+                out.append({"config": cid, "k": k, "per_vertex": pv, "total": str(total),
+                            "matches_reference": (str(total) == gold) if gold else None,
+                            "strategy": STRAT_NAMES[strat], "n": h.n, "m": m,
+                            "rank_ms": rank_ms, "direct_ms": direct_ms, "count_ms": cms,
+                            "cliques_per_s": total / (cms / 1e3) if cms else None,
+                            "oriented_edges_per_s": m / (step / 1e3),
+                            "build_s": build_s})
+        h.close()
+    return out
+
+
 def run_kcg(args):
     import torch
     import torch.distributed as dist
@@ -369,6 +412,13 @@ def run_kcg(args):
                 ent["reference_threads"] = ref["threads"]
         secondary[f"peel_approx_k{k}"] = ent
 
+    # every BASELINE config at every k (SURVEY.md §8(d) units): device-timed
+    # phases, cliques/s of the count and oriented edges/s of the step; the
+    # graphs are the canonical generators' (config 5 built on the device)
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = config_sweep(kcg, args.config)
+
     # e2e: the reference-facing C ABI with host buffers (pinned), H2D + D2H
     # inside the timed region
     e2e = None
@@ -426,6 +476,7 @@ def run_kcg(args):
             "clocks": clk,
             "count_stats": stats,
             "secondary": secondary,
+            "configs": sweep,
         }
         print(json.dumps(line))
     h.close()
