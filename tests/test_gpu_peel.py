@@ -142,3 +142,54 @@ def test_peel_config_goldens():
         assert f"{gen.digest_u32(out['dense_vertices']):016x}" == ent["dense_digest"], key
         if ent["exact"]:
             assert f"{gen.digest_u64(out['core']):016x}" == ent["core_digest"], key
+
+
+def test_update_counts_random_states_vs_port(port):
+    """Arbitrary peeled sets and (even inconsistent) counts: the device's
+    two-sided restricted recount equals the C restatement's recount
+    differencing, which is the reference's semantics for any input."""
+    rng = np.random.default_rng(77)
+    for trial in range(12):
+        g = gen.gnp(int(rng.integers(10, 60)), float(rng.uniform(0.2, 0.6)), 900 + trial)
+        k = int(rng.integers(2, 6))
+        peeled = (rng.random(g.n) < 0.3).astype(np.uint8)
+        live = np.flatnonzero(peeled == 0)
+        if len(live) == 0:
+            continue
+        batch = np.sort(rng.choice(live, size=min(len(live), int(rng.integers(1, 6))),
+                                   replace=False))
+        counts = rng.integers(0, 2000, size=g.n).astype(np.uint64)
+        c_gpu, c_port = counts.copy(), counts.copy()
+        with oriented(g) as h:
+            try:
+                r_gpu = h.update_counts(k, c_gpu, batch, peeled)
+                err_gpu = None
+            except kcg.KcgLogicError:
+                r_gpu, err_gpu = None, "logic"
+        try:
+            r_port = port.update_counts(g, k, c_port, batch, peeled)
+            err_port = None
+        except Exception:  # noqa: BLE001 - status 4 from the port
+            r_port, err_port = None, "logic"
+        assert err_gpu == err_port, trial
+        if err_gpu is None:
+            assert r_gpu[0] == r_port[0] and r_gpu[1].tolist() == r_port[1].tolist(), trial
+        assert c_gpu.tolist() == c_port.tolist(), trial
+
+
+def test_peel_random_graphs_vs_port(port):
+    rng = np.random.default_rng(5)
+    for trial in range(8):
+        g = gen.gnp(int(rng.integers(15, 70)), float(rng.uniform(0.2, 0.5)), 4400 + trial)
+        for k in (2, 3, 4):
+            with oriented(g, kcg.BARENBOIM_ELKIN, 0.5) as h:
+                ex = h.peel_exact(k)
+                ap = h.peel_approx(k, 0.3)
+            pex = port.peel(g, k, True)
+            pap = port.peel(g, k, False, 0.3)
+            for a, b in ((ex, pex), (ap, pap)):
+                assert a["rounds"] == b["rounds"] and a["best_round"] == b["best_round"]
+                assert a["total_cliques"] == b["total_cliques"]
+                assert float(a["best_density"]).hex() == float(b["best_density"]).hex()
+                assert a["dense_vertices"].tolist() == b["dense_vertices"].tolist()
+            assert ex["core"].tolist() == pex["core"].tolist()
