@@ -182,19 +182,26 @@ __global__ void __launch_bounds__(512)
     const uint64_t wr0 = rdag_off[ru];
     const uint32_t dout = uint32_t(rdag_off[ru + 1] - wr0);
     uint32_t got = 0;
-    for (uint64_t p0 = b; p0 < e && got < dout; p0 += 512) {
-      const uint64_t p = p0 + threadIdx.x;
-      uint32_t v = 0, rv = 0, out = 0;
-      if (p < e) {
-        v = adj[p];
-        rv = rank[v];
-        out = rv > ru;
+    // 2048 entries per step, four consecutive ones per thread (blocked
+    // arrangement, loads in flight before the gathers)
+    for (uint64_t p0 = b; p0 < e && got < dout; p0 += 4 * 512) {
+      const uint64_t pb = p0 + 4 * threadIdx.x;
+      uint32_t v[4], rv[4], out[4], at[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = pb + j < e ? adj[pb + j] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        rv[j] = v[j] != 0xffffffffu ? rank[v[j]] : 0u;
+        out[j] = v[j] != 0xffffffffu && rv[j] > ru;
       }
-      uint32_t at, tot;
+      uint32_t tot;
       Scan(tmp).ExclusiveSum(out, at, tot);
-      if (out) {
-        if (dag_adj) dag_adj[wid + got + at] = v;
-        rdag_adj[wr0 + got + at] = rv;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (out[j]) {
+          if (dag_adj) dag_adj[wid + got + at[j]] = v[j];
+          rdag_adj[wr0 + got + at[j]] = rv[j];
+        }
       }
       got += tot;
       __syncthreads();
