@@ -164,3 +164,32 @@ def test_kcore_exact_matches_reference():
     with kcg.DeviceGraph.from_graph(g) as h:
         r, _, _ = h.rank(kcg.KCORE)
     assert f"{gen.digest_u32(r):016x}" == g4["rank_digest"]
+
+
+def test_concurrent_handles_from_host_threads():
+    """SURVEY.md §8(b) threading: one handle per host thread (each with its
+    own streams, recycled through the handle pool) gives identical results
+    when the calls overlap."""
+    import threading
+    g = gen.rmat(12, 1 << 15, seed=7, permute=True)
+    with kcg.DeviceGraph.from_graph(g) as h:
+        want = h.pipeline(kcg.BARENBOIM_ELKIN, 0.5, 4, per_vertex=True)
+    results, errors = [], []
+
+    def work():
+        try:
+            for _ in range(5):
+                with kcg.DeviceGraph.from_graph(g) as hh:
+                    results.append(hh.pipeline(kcg.BARENBOIM_ELKIN, 0.5, 4, per_vertex=True))
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work) for _ in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(results) == 30
+    for total, pv in results:
+        assert total == want[0] and np.array_equal(pv, want[1])
