@@ -26,3 +26,17 @@ def test_reference_acceptance_criterion(criterion):
         return
     assert r.returncode == 0, out
     assert out.splitlines()[-1].startswith("PASS"), out
+
+
+def test_reference_unit_tests():
+    """The reference's own unit tests (proj/tests/test_graph.cpp,
+    test_orientation.cpp, test_counting.cpp, test_oracle.cpp,
+    test_sampling.cpp, test_bucket_queue.cpp, test_peeling.cpp; unmodified)
+    built over tests/cpp/doctest_shim and linked with libkclique_b200.so."""
+    binp = os.path.join(ROOT, "tests", "cpp", "bin", "unit_b200")
+    if not os.path.exists(binp):
+        pytest.skip("unit_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=1800)
+    out = (r.stdout + r.stderr).strip()
+    assert r.returncode == 0, out[-4000:]
+    assert "0 failed | assertions" in out, out[-4000:]
