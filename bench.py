@@ -45,6 +45,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the per-config sweep reported under `configs`")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip the instrumented config-5 block")
     ap.add_argument("--cpu-budget-s", type=float, default=240.0,
                     help="wall budget for the reference arm's timed steps")
     return ap.parse_args()
@@ -141,12 +143,70 @@ def measured_peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def alg_bytes(n, out_off, out_adj):
-    """B_alg = 16n + 20m + 4 * sum_w indeg(w) * outdeg(w)."""
-    outdeg = np.diff(out_off).astype(np.float64)
-    indeg = np.bincount(out_adj, minlength=n).astype(np.float64)
-    m = len(out_adj)
-    return 16.0 * n + 20.0 * m + 4.0 * float(np.dot(indeg, outdeg))
+def counting_peaks():
+    """The §8(d) roof denominators: HBM from MEASURED_PEAKS.json (driver-
+    measured copy), L2 read bandwidth and the POPC issue rate from our own
+    microbenchmark on the B200 (tools/peaks/peaks.cu -> profiles/r02_peaks.json:
+    LDG.128 sweeps over 16-96 MB working sets; POPC at 16 lanes per SM per
+    clock, one eighth of LOP3/IADD3)."""
+    hbm, hbm_src = measured_peaks()
+    p = {"hbm_gbs": hbm, "hbm_source": hbm_src}
+    path = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        iss = d["issue"]
+        p.update({"l2_gbs": float(d["l2_read_gbs"]),
+                  "popc_lane_ops_per_s": float(iss["popc"]["lane_ops_per_s"]),
+                  "popc_warp_inst_per_sm_cycle": float(iss["popc"]["warp_inst_per_sm_cycle"]),
+                  "peaks_source": "measured (profiles/r02_peaks.json, tools/peaks/peaks.cu)"})
+    return p
+
+
+def ops_table():
+    """OPS(k) of SURVEY.md §8(d) (one AND + one POPC per bitmap word of every
+    intersection the reference's edge engine performs): tools/kc_ops.c, an
+    instrumented restatement of clique_rec.hpp:24-62, totals cross-checked
+    against the goldens (profiles/r01_ops_k.jsonl)."""
+    out = {}
+    path = os.path.join(ROOT, "profiles", "r01_ops_k.jsonl")
+    if os.path.exists(path):
+        for line in open(path):
+            d = json.loads(line)
+            out[(d["config"], d["k"])] = int(d["ops"])
+    return out
+
+
+def roofline_entry(cid, k, n, m, sum_io, count_ms, peaks, ops, l2_bytes, per_vertex=False,
+                   t3=None):
+    """SURVEY.md §8(d) roof selection for one (config, k) count:
+    T_roof = max(B_alg / BW, (OPS / 2) / P_popc), BW = measured L2 when the
+    DAG (8(n+1) + 4m bytes) fits in L2, else measured HBM; OPS counts an AND
+    and a POPC per word, and POPC (16 lanes/SM/clk) is the binding integer
+    pipe.  frac = T_roof / T_measured."""
+    b_alg = 16.0 * n + 20.0 * m + 4.0 * sum_io
+    if per_vertex and t3 is not None:
+        b_alg += 16.0 * (t3 + 2.0 * m)  # u64 per-vertex atomics (§8(d))
+    dag_bytes = 8.0 * (n + 1) + 4.0 * m
+    fits = bool(l2_bytes) and dag_bytes <= l2_bytes and "l2_gbs" in peaks
+    bw = peaks["l2_gbs"] if fits else peaks["hbm_gbs"]
+    t_bytes = b_alg / (bw * 1e9)
+    op = None if per_vertex else ops.get((cid, k))
+    t_ops = (op / 2.0) / peaks["popc_lane_ops_per_s"] \
+        if op and "popc_lane_ops_per_s" in peaks else None
+    t = count_ms / 1e3
+    e = {"alg_bytes": b_alg, "dag_bytes": dag_bytes, "bw_roof": "l2" if fits else "hbm",
+         "bw_peak_gbs": bw, "t_bytes_ms": t_bytes * 1e3,
+         "ops": op, "t_issue_ms": t_ops * 1e3 if t_ops else None,
+         "count_ms": count_ms}
+    if t_ops and t_ops > t_bytes:
+        e.update({"bound": "int_issue_popc", "achieved": (op / 2.0) / t / 1e12,
+                  "peak": peaks["popc_lane_ops_per_s"] / 1e12, "unit": "Tpopc/s"})
+    else:
+        e.update({"bound": e["bw_roof"], "achieved": b_alg / t / 1e9, "peak": bw,
+                  "unit": "GB/s"})
+    e["frac"] = max(t_bytes, t_ops or 0.0) / t
+    e["hbm_frac"] = b_alg / t / 1e9 / peaks["hbm_gbs"]
+    return e
 
 
 def ncu_entry(cfg_id, k):
@@ -192,7 +252,9 @@ def run_reference(args):
     rg = R.graph(g)
     # first step doubles as warm-up and sizes the run to the budget
     total, t_first = reference_step(R, rg, g, spec, k)
-    warm = max(0, min(args.warmup, 1) - 1)
+    # the same number of warm-up steps as the B200 arm (>= 3); the first
+    # step counts as one
+    warm = max(args.warmup, 3) - 1
     for _ in range(warm):
         reference_step(R, rg, g, spec, k)
     steps = max(1, min(args.steps, int(args.cpu_budget_s // max(t_first, 1e-3))))
@@ -209,7 +271,7 @@ def run_reference(args):
         "impl": "reference", "metric": f"k-cliques/s (k={k})", "value": value,
         "unit": "cliques/s", "n_gpus": world, "steps": steps, "warmup": 1 + warm,
         "requested_steps": args.steps, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32 ids / u64 counts",
+        "scaling": "strong", "warmup_steps_run": 1 + warm, "vs_baseline": None, "dtype": "u32 ids / u64 counts",
         "data": "synthetic (in-repo deterministic generator)",
         "config": config_obj(args.config, spec, k, g),
         "cpu_baseline": {"value": value, "unit": "cliques/s", "cores": cores, "kind": kind,
@@ -240,45 +302,142 @@ def cpu_baseline(g, spec, k):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
-def config_sweep(kcg, skip_cfg):
+def config_sweep(kcg, peaks, ops, l2_bytes):
     """One line per (config, k[, per-vertex]) with the reference goldens'
-    verdict (tests/golden/config*.json)."""
+    verdict (tests/golden/config*.json) and the §8(d) roofline of the count.
+    Config 5 is left to config5_block (its own e2e and roofline)."""
     out = []
-    for cid in (1, 2, 3, 4, 5):
+    for cid in (1, 2, 3, 4):
         spec = gen.CONFIGS[cid]
         strat = gen.gpu_strategy(spec)
         gpath = os.path.join(ROOT, "tests", "golden", f"config{cid}.json")
         golden = json.load(open(gpath)) if os.path.exists(gpath) else {}
         t0 = time.perf_counter()
-        if cid == 5:
-            p = spec["rmat"]
-            h = kcg.DeviceGraph.rmat(p["scale"], p["samples"], seed=p["seed"],
-                                     permute=p["permute"])
-        else:
-            h = kcg.DeviceGraph.from_graph(gen.load_config_graph(cid, cache=False))
+        h = kcg.DeviceGraph.from_graph(gen.load_config_graph(cid, cache=False))
         build_s = time.perf_counter() - t0
         h.rank(strat, spec["eps"], download=False)
         rank_ms = h.timings()["rank_ms"]
         h.direct(download=False)
         direct_ms = h.timings()["direct_ms"]
         m = h.m
+        sum_io = h.dag_work()
+        t3 = None
         for k in spec["ks"]:
             for pv in ([False, True] if k in spec["pv_ks"] else [False]):
-                if cid != 5:
-                    h.count(k, per_vertex=pv)  # warm
+                if pv and t3 is None:
+                    t3, _ = h.count(3)
+                h.count(k, per_vertex=pv)  # warm
                 total, _ = h.count(k, per_vertex=pv)
-                cms = h.timings()["count_ms"]
+                tm = h.timings()
+                cms = tm["count_ms"]
                 step = rank_ms + direct_ms + cms
-                gold = golden.get("counts", {}).get(str(k), {}).get("total")
+                gold = (golden.get("per_vertex" if pv else "counts", {}).get(str(k), {})
+                        .get("total"))
                 out.append({"config": cid, "k": k, "per_vertex": pv, "total": str(total),
                             "matches_reference": (str(total) == gold) if gold else None,
                             "strategy": STRAT_NAMES[strat], "n": h.n, "m": m,
                             "rank_ms": rank_ms, "direct_ms": direct_ms, "count_ms": cms,
                             "cliques_per_s": total / (cms / 1e3) if cms else None,
                             "oriented_edges_per_s": m / (step / 1e3),
+                            "roofline": roofline_entry(cid, k, h.n, m, sum_io,
+                                                       tm["count_kernel_ms"], peaks, ops,
+                                                       l2_bytes, pv, t3),
                             "build_s": build_s})
         h.close()
     return out
+
+
+def config5_block(kcg, peaks, ops, l2_bytes, steps=2):
+    """Config 5 (R-MAT s24, EF32, degree order; k=4 totals and per-vertex
+    counts) measured like the headline: device-timed phases with the graph
+    resident in HBM, and e2e through the C ABI from a pinned HOST CSR
+    (kcg_graph_create H2D + kcg_pipeline + per-vertex D2H inside the timed
+    region), the §8(d) roofline (HBM: the 2 GB DAG exceeds L2) and the
+    reference's time from the committed offline golden run."""
+    import torch
+
+    spec = gen.CONFIGS[5]
+    p = spec["rmat"]
+    gpath = os.path.join(ROOT, "tests", "golden", "config5.json")
+    golden = json.load(open(gpath)) if os.path.exists(gpath) else {}
+    t0 = time.perf_counter()
+    hd = kcg.DeviceGraph.rmat(p["scale"], p["samples"], seed=p["seed"], permute=p["permute"])
+    build_s = time.perf_counter() - t0
+    off, adj = hd.csr()
+    hd.close()
+    off_p = torch.from_numpy(off.view(np.int64)).pin_memory()
+    adj_p = torch.from_numpy(adj.view(np.int32)).pin_memory()
+    del off, adj
+    n = off_p.numel() - 1
+    strat = gen.gpu_strategy(spec)
+    blk = {"workload": "config5: " + spec["desc"], "k": 4, "n": n,
+           "m": adj_p.numel() // 2, "strategy": STRAT_NAMES[strat],
+           "device_build_s": build_s}
+    # device-resident phases (graph uploaded once)
+    h = kcg.DeviceGraph.from_csr_ptr(n, off_p.data_ptr(), adj_p.data_ptr())
+    h.rank(strat, spec["eps"], download=False)
+    rank_ms = h.timings()["rank_ms"]
+    h.direct(download=False)
+    direct_ms = h.timings()["direct_ms"]
+    m = h.m
+    sum_io = h.dag_work()
+    t3, _ = h.count(3)
+    for pv in (False, True):
+        key = "per_vertex" if pv else "totals"
+        cms, kms = [], []
+        total = None
+        for _ in range(steps):
+            total, _ = h.count(4, per_vertex=pv)
+            tm = h.timings()
+            cms.append(tm["count_ms"])
+            kms.append(tm["count_kernel_ms"])
+        cm, km = sum(cms) / len(cms), sum(kms) / len(kms)
+        gold = golden.get("per_vertex" if pv else "counts", {}).get("4", {})
+        blk[key] = {"total": str(total),
+                    "matches_reference": (str(total) == gold.get("total")) if gold else None,
+                    "rank_ms": rank_ms, "direct_ms": direct_ms, "count_ms": cm,
+                    "step_ms": rank_ms + direct_ms + cm,
+                    "cliques_per_s": total / (cm / 1e3),
+                    "oriented_edges_per_s": m / ((rank_ms + direct_ms + cm) / 1e3),
+                    "roofline": roofline_entry(5, 4, n, m, sum_io, km, peaks, ops, l2_bytes,
+                                               pv, t3)}
+        ncu = ncu_entry(5, 4) if not pv else None
+        if ncu:
+            blk[key]["roofline"]["traffic"] = ncu.get("dram_bytes_per_launch")
+            blk[key]["roofline"]["l2_traffic"] = ncu.get("l2_bytes_per_launch")
+        if gold.get("t_count_s"):
+            ref_s = gold["t_count_s"] + golden.get("t_rank_s", 0) + golden.get("t_direct_s", 0)
+            blk[key]["cpu_baseline"] = {
+                "value": int(gold["total"]) / gold["t_count_s"], "unit": "cliques/s",
+                "cores": golden.get("threads"), "kind": "reference",
+                "sample": "OFFLINE: the unmodified reference's make_ranking + "
+                          "direct_by_ranking + count_%s on this config in the build "
+                          "container (tests/golden/config5.json, %.0f s count, %.0f s "
+                          "step); too long to rerun in the bench" % (key, gold["t_count_s"],
+                                                                    ref_s)}
+    h.close()
+    # e2e through the C ABI with host buffers, every step: H2D of the CSR,
+    # rank + orient + count on the device, D2H of the result
+    for pv in (False, True):
+        key = "per_vertex" if pv else "totals"
+        times = []
+        total = None
+        for i in range(steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            he = kcg.DeviceGraph.from_csr_ptr(n, off_p.data_ptr(), adj_p.data_ptr())
+            total, _ = he.pipeline(strat, spec["eps"], 4, per_vertex=pv)
+            he.close()
+            dt = time.perf_counter() - t0
+            if i:
+                times.append(dt)
+        esec = sum(times) / len(times)
+        blk[key]["e2e"] = {"value": total / esec, "unit": "cliques/s", "ms_per_step": esec * 1e3,
+                           "h2d_bytes_per_step": int(off_p.numel() * 8 + adj_p.numel() * 4),
+                           "d2h_bytes_per_step": 8 + (8 * n if pv else 0),
+                           "path": "kcg_graph_create(pinned host CSR) + kcg_pipeline%s + "
+                                   "destroy" % (" (per-vertex, D2H)" if pv else "")}
+    return blk
 
 
 def run_kcg(args):
@@ -297,13 +456,22 @@ def run_kcg(args):
     h = kcg.DeviceGraph.from_graph(g)
     stream = torch.cuda.ExternalStream(h.stream_ptr())
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    red = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     def step():
         if world == 1:
             return h.pipeline(strat, eps, k)[0]
+        # one GPU's share: replicated rank + DAG, its work-balanced source
+        # range, then the all-reduce of the u64 total (on the library
+        # stream, so the step's events cover it)
         h.rank(strat, eps, download=False)
         h.direct(download=False)
-        return h.count_part(k, rank, world)[0]
+        b = h.partition_plan(k, world)
+        t, _ = h.count_range(k, int(b[rank]), int(b[rank + 1]))
+        with torch.cuda.stream(stream):
+            red.fill_(int(np.uint64(t).view(np.int64)))
+            dist.all_reduce(red)
+        return None
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -316,12 +484,12 @@ def run_kcg(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     phase = {"rank_ms": 0.0, "direct_ms": 0.0, "count_ms": 0.0, "count_kernel_ms": 0.0}
-    part_total = 0
+    total = None
     for i in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()
         ev[i][0].record(stream)
-        part_total = step()
+        total = step()
         ev[i][1].record(stream)
         t = h.timings()
         for key in phase:
@@ -330,13 +498,11 @@ def run_kcg(args):
     launches = h.timings()["launches"] - launches0
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    total = part_total
     if world > 1:
+        total = int(np.int64(red.item()).view(np.uint64))
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-        from paper_2002_10047_b200 import shard
-        total, _ = shard.allreduce_counts(part_total, None, device="cuda")
         dist.barrier()
     ms_per_step = ms / args.steps
     value = total / (ms_per_step / 1e3)
@@ -344,30 +510,26 @@ def run_kcg(args):
         phase[key] /= args.steps
     stats = h.count_stats()
 
-    # roofline of the dominant (counting) kernels
-    off, adj, max_out = h.direct()
-    b_alg = alg_bytes(g.n, off, adj)
-    peak, peak_src = measured_peaks()
-    achieved = b_alg / (phase["count_kernel_ms"] / 1e3) / 1e9
-    dag_bytes = 8 * (g.n + 1) + 4 * g.m
+    # roofline of the dominant (counting) kernels, SURVEY.md §8(d)
+    peaks = counting_peaks()
+    ops = ops_table()
+    l2_bytes = kcg.device_info().get("l2_bytes", 0)
+    sum_io = h.dag_work()
+    roofline = roofline_entry(args.config, k, g.n, g.m, sum_io, phase["count_kernel_ms"],
+                              peaks, ops, l2_bytes)
     ncu = ncu_entry(args.config, k)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak,
-                "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
-                "alg_bytes_per_launch": b_alg, "kernel_ms": phase["count_kernel_ms"],
-                "peak_source": peak_src,
-                "note": "achieved = B_alg (SURVEY.md §8(d): 16n+20m+4*sum indeg*outdeg) / "
-                        "device time of the counting kernels; the DAG (%.0f MB) %s L2"
-                        % (dag_bytes / 1e6, "fits in" if dag_bytes < 126e6 else "exceeds")}
-    if ncu and "sm_throughput_pct_time_weighted" in ncu:
-        # the limiting roof of the L2-resident counting kernels is integer
-        # issue: ncu's SM throughput = achieved fraction of
-        # peak issue, time-weighted over the launches of one count
-        roofline["issue"] = {
-            "frac": ncu["sm_throughput_pct_time_weighted"] / 100.0,
-            "ipc": ncu["ipc_time_weighted"], "peak_ipc": ncu["issue_slot_peak_ipc"],
-            "threads_per_inst": ncu["threads_per_inst_time_weighted"],
-            "source": "profiles/ncu_summary.json: " + ncu["source"]}
+    roofline.update({
+        "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
+        "l2_traffic": ncu.get("l2_bytes_per_launch") if ncu else None,
+        "kernel_ms": phase["count_kernel_ms"], "peaks": peaks,
+        "note": "achieved = B_alg (16n+20m+4*sum indeg*outdeg) / device time of the counting "
+                "kernels (CUDA events on the library stream); BW = measured L2 read bandwidth "
+                "because the DAG fits the 126 MB L2 (SURVEY.md §8(d)); hbm_frac = the same "
+                "bytes against measured HBM; traffic = ncu dram bytes of one count"})
+    if ncu and "smem_wavefront_floor_ms" in ncu:
+        roofline["smem"] = {k2: ncu[k2] for k2 in ("smem_wavefronts", "smem_wavefront_floor_ms",
+                                                    "sm_throughput_pct_time_weighted")
+                            if k2 in ncu}
 
     # secondary: the config's other k values on the same DAG (counting only)
     secondary = {}
@@ -379,14 +541,18 @@ def run_kcg(args):
             h.direct(download=False)
             reps = 3
             tot2 = 0
-            cms = 0.0
+            cms = kms = 0.0
             for _ in range(reps):
                 tot2, _ = h.count(k2)
                 cms += h.timings()["count_ms"]
+                kms += h.timings()["count_kernel_ms"]
             cms /= reps
+            kms /= reps
             secondary[f"k{k2}"] = {"total": str(tot2), "count_ms": cms,
                                    "cliques_per_s": tot2 / (cms / 1e3),
-                                   "oriented_edges_per_s": g.m / (cms / 1e3)}
+                                   "oriented_edges_per_s": g.m / (cms / 1e3),
+                                   "roofline": roofline_entry(args.config, k2, g.n, g.m, sum_io,
+                                                              kms, peaks, ops, l2_bytes)}
 
     # downstream consumer of the per-vertex counts:
     # approximate k-clique densest-subgraph peeling on the same handle
@@ -412,12 +578,13 @@ def run_kcg(args):
                 ent["reference_threads"] = ref["threads"]
         secondary[f"peel_approx_k{k}"] = ent
 
-    # every BASELINE config at every k (SURVEY.md §8(d) units): device-timed
-    # phases, cliques/s of the count and oriented edges/s of the step; the
-    # graphs are the canonical generators' (config 5 built on the device)
-    sweep = None
+    # every other BASELINE config at every k (SURVEY.md §8(d) units) with its
+    # roofline; config 5 gets its own fully instrumented block
+    sweep = c5 = None
     if world == 1 and not args.no_sweep:
-        sweep = config_sweep(kcg, args.config)
+        sweep = config_sweep(kcg, peaks, ops, l2_bytes)
+    if world == 1 and not args.no_config5:
+        c5 = config5_block(kcg, peaks, ops, l2_bytes)
 
     # e2e: the reference-facing C ABI with host buffers (pinned), H2D + D2H
     # inside the timed region
@@ -464,8 +631,14 @@ def run_kcg(args):
             "vs_baseline": None, "dtype": "u32 ids / u64 counts",
             "data": "synthetic (in-repo deterministic generator, seeded)",
             "config": config_obj(args.config, spec, k, g,
-                                 {"parallelism": f"sources r % {world}" if world > 1
-                                  else "single GPU"}),
+                                 {"parallelism": "work-balanced contiguous source ranges "
+                                                 "(kcg_partition_plan) + NCCL all-reduce, "
+                                                 f"{world} GPUs" if world > 1
+                                  else "single GPU",
+                                  "reference_arm": "the driver's --impl reference arm runs "
+                                                   "this same config (config 2) on the host "
+                                                   "cores; config 5's reference time is the "
+                                                   "committed offline run (config5 block)"}),
             "total": str(total),
             "oriented_edges_per_s": g.m / (ms_per_step / 1e3),
             "phases_ms": phase,
@@ -475,6 +648,7 @@ def run_kcg(args):
             "gpu_launches": launches,
             "clocks": clk,
             "count_stats": stats,
+            "config5": c5,
             "secondary": secondary,
             "configs": sweep,
         }

@@ -144,10 +144,28 @@ int kcg_direct(kcg_graph* g, uint64_t* out_offsets, uint32_t* out_targets,
  * NULL for totals only, else n entries indexed by vertex id.
  * KCG_EINVAL for k < 2. */
 int kcg_count(kcg_graph* g, int k, uint64_t* total, uint64_t* per_vertex);
-/* Multi-GPU sharding: counts only the cliques whose
- * lowest-ranked vertex r satisfies r % nparts == part.  Summing the
- * totals (and per-vertex arrays) of all parts gives kcg_count's result;
- * callers all-reduce them across GPUs.  per_vertex is NULL or n entries. */
+/* Multi-GPU sharding (the reference's edge engine over
+ * independent sources, proj/src/counting.cpp:138-198).  Every clique is
+ * charged to its lowest-ranked vertex r (rank space), so source ranges
+ * partition the cliques.
+ * kcg_partition_plan: work-balanced contiguous ranges -- bounds[0..nparts],
+ *   part p owns ranks [bounds[p], bounds[p+1]); the work of source r is
+ *   1 + d + sum_{x in N+(r)} (1 + d+(x)) (+ d^2 for k >= 5), the staging
+ *   term of the counting kernels (paper_2002_10047_b200/shard.py:plan is
+ *   the host mirror).
+ * kcg_count_range: the cliques whose lowest-ranked vertex lies in
+ *   [r_lo, r_hi).
+ * kcg_count_part: kcg_count_range over part `part` of kcg_partition_plan.
+ * Summing the totals (and per-vertex arrays) of all parts gives kcg_count's
+ * result; callers all-reduce them across GPUs.  per_vertex is NULL or n
+ * entries.  KCG_EINVAL for k < 2, part >= nparts or r_lo > r_hi. */
+int kcg_partition_plan(kcg_graph* g, int k, uint32_t nparts, uint32_t* bounds);
+/* sum_w indeg(w) * outdeg(w) over the current DAG: the staging term of the
+ * per-source scheme's algorithmic bytes (SURVEY.md §8(d) B_alg = 16n + 20m
+ * + 4 * this), computed on the device (bench.py's roofline). */
+int kcg_dag_work(kcg_graph* g, uint64_t* sum_indeg_outdeg);
+int kcg_count_range(kcg_graph* g, int k, uint32_t r_lo, uint32_t r_hi,
+                    uint64_t* total, uint64_t* per_vertex);
 int kcg_count_part(kcg_graph* g, int k, uint32_t part, uint32_t nparts,
                    uint64_t* total, uint64_t* per_vertex);
 /* Device pointer to the per-vertex counts of the last per-vertex count

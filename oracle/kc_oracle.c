@@ -309,13 +309,15 @@ uint64_t kco_alg_bytes(uint32_t n, const uint64_t* out_off, const uint32_t* out_
   return 16 * (uint64_t)n + 20 * m + 4 * s;
 }
 
-/* The multi-GPU split of kcg_count_part, restated for the CPU tests: only
- * the cliques whose lowest-ranked vertex v has rank[v] % nparts == part
- * (edge tasks (v,u) of counting.cpp:158-187 with such a source v). */
-int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
-                   const uint32_t* rank, int k, uint32_t part, uint32_t nparts,
-                   uint64_t* total_out, uint64_t* pv) {
-  if (k < 2 || nparts == 0 || part >= nparts) return 1;
+/* The multi-GPU split, restated for the CPU tests: only
+ * the cliques whose lowest-ranked vertex v passes the source filter -- the
+ * edge tasks (v,u) of counting.cpp:158-187 with such a source v.
+ * mode 0: rank[v] % nparts == part (kco_count_part);
+ * mode 1: lo <= rank[v] < hi (kco_count_range, the contiguous ranges of
+ * kcg_partition_plan / shard.plan). */
+static int kco_count_sources(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
+                             const uint32_t* rank, int k, int mode, uint32_t a0, uint32_t a1,
+                             uint64_t* total_out, uint64_t* pv) {
   uint64_t total = 0;
   if (pv) memset(pv, 0, (size_t)n * 8);
   uint64_t maxd = 0;
@@ -332,7 +334,7 @@ int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
   for (int i = 0; i < k + 3; i++) c.bufs[i] = malloc((maxd + 1) * 4);
   uint64_t next_token = 1;
   for (uint32_t v = 0; v < n; v++) {
-    if (rank[v] % nparts != part) continue;
+    if (mode == 0 ? rank[v] % a1 != a0 : (rank[v] < a0 || rank[v] >= a1)) continue;
     for (uint64_t e = out_off[v]; e < out_off[v + 1]; e++) {
       uint32_t u = out_adj[e];
       if (k == 2) {
@@ -361,6 +363,20 @@ int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
   for (int i = 0; i < k + 3; i++) free(c.bufs[i]);
   free(c.bufs), free(c.chain), free(c.stamp);
   return 0;
+}
+
+int kco_count_part(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
+                   const uint32_t* rank, int k, uint32_t part, uint32_t nparts,
+                   uint64_t* total_out, uint64_t* pv) {
+  if (k < 2 || nparts == 0 || part >= nparts) return 1;
+  return kco_count_sources(n, out_off, out_adj, rank, k, 0, part, nparts, total_out, pv);
+}
+
+int kco_count_range(uint32_t n, const uint64_t* out_off, const uint32_t* out_adj,
+                    const uint32_t* rank, int k, uint32_t r_lo, uint32_t r_hi,
+                    uint64_t* total_out, uint64_t* pv) {
+  if (k < 2 || r_lo > r_hi) return 1;
+  return kco_count_sources(n, out_off, out_adj, rank, k, 1, r_lo, r_hi, total_out, pv);
 }
 
 /* ---- peeling --------------------------------- */

@@ -4,5 +4,3 @@ import os
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_ROOT = os.path.dirname(PKG_DIR)
 LIB_DIR = os.path.join(PKG_DIR, "lib")
-ORACLE_DIR = os.path.join(REPO_ROOT, "oracle")
-ORACLE_REF_DIR = os.path.join(ORACLE_DIR, "_ref")

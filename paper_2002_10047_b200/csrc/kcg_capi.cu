@@ -45,6 +45,12 @@ __global__ void bijection_kernel(const uint32_t* __restrict__ rank, uint32_t n,
 }  // namespace
 
 void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s) {
+  const Device& d = device();
+  if (d.pool) return cudaMallocFromPoolAsync(p, bytes, d.pool, s);
+  return cudaMallocAsync(p, bytes, s);
+}
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 const Device& device() {
@@ -69,11 +75,19 @@ const Device& device() {
     g_dev.l2 = p.l2CacheSize;
     g_dev.major = p.major;
     g_dev.minor = p.minor;
-    // keep freed pool memory cached: handles come and go on every call
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    // a library-owned pool that keeps freed memory cached (handles come and
+    // go on every drop-in call); the host application's default pool is
+    // left as it was
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    if (cudaMemPoolCreate(&g_dev.pool, &pp) == cudaSuccess) {
       uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      cudaMemPoolSetAttribute(g_dev.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    } else {
+      g_dev.pool = nullptr;
     }
     (void)cudaGetLastError();
     if (p.major != 10) {
@@ -217,19 +231,11 @@ const Graph* G(const kcg_graph* h) {
   return reinterpret_cast<const Graph*>(h);
 }
 
-// Copies host -> device through a pinned staging buffer when the source is
-// pageable (one cudaMemcpyAsync per chunk).
+// Stream-ordered host -> device copy on the handle's stream (a pageable
+// source is staged by the driver before the call returns).
 void upload(Graph& g, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
-  cudaPointerAttributes attr;
-  bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
-                attr.type == cudaMemoryTypeHost;
-  (void)cudaGetLastError();
-  if (pinned) {
-    KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
-  } else {
-    KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
-  }
+  KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
   g.times.h2d_bytes += bytes;
 }
 
@@ -266,6 +272,35 @@ void install_rank_device(Graph& g) {
   g.has_dag = g.has_rdag = false;
 }
 
+int count_range_impl(kcg_graph* h, int k, bool plan, uint32_t part, uint32_t nparts,
+                     uint32_t r_lo, uint32_t r_hi, uint64_t* total, uint64_t* per_vertex) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (plan && (nparts == 0 || part >= nparts)) fail(KCG_EINVAL, "part must be < nparts");
+    if (!plan && r_lo > r_hi) fail(KCG_EINVAL, "source range must have r_lo <= r_hi");
+    if (!g.has_rdag) {
+      if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
+      build_dag(g, false);
+    }
+    if (plan) {
+      std::vector<uint32_t> b(size_t(nparts) + 1);
+      partition_plan(g, k, nparts, b.data());
+      r_lo = b[part];
+      r_hi = b[part + 1];
+    }
+    g.times.d2h_bytes = 0;
+    uint64_t t = count_cliques(g, k, per_vertex != nullptr, r_lo, r_hi);
+    if (per_vertex) {
+      g.mark(4);
+      download(g, per_vertex, g.pv.p, size_t(g.n) * 8);
+      g.mark(5);
+      g.sync();
+      g.times.download_ms = g.elapsed(4, 5);
+    }
+    if (total) *total = t;
+  });
+}
 }  // namespace
 }  // namespace kcg
 
@@ -518,26 +553,39 @@ int kcg_count(kcg_graph* h, int k, uint64_t* total, uint64_t* per_vertex) {
   });
 }
 
-int kcg_count_part(kcg_graph* h, int k, uint32_t part, uint32_t nparts, uint64_t* total,
-                   uint64_t* per_vertex) {
+int kcg_partition_plan(kcg_graph* h, int k, uint32_t nparts, uint32_t* bounds) {
   return guarded([&] {
     Graph& g = *G(h);
     if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
+    if (!bounds) fail(KCG_EINVAL, "null bounds");
     if (!g.has_rdag) {
       if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
       build_dag(g, false);
     }
-    g.times.d2h_bytes = 0;
-    uint64_t t = count_cliques(g, k, per_vertex != nullptr, part, nparts);
-    if (per_vertex) {
-      g.mark(4);
-      download(g, per_vertex, g.pv.p, size_t(g.n) * 8);
-      g.mark(5);
-      g.sync();
-      g.times.download_ms = g.elapsed(4, 5);
-    }
-    if (total) *total = t;
+    partition_plan(g, k, nparts, bounds);
   });
+}
+
+int kcg_dag_work(kcg_graph* h, uint64_t* sum_indeg_outdeg) {
+  return guarded([&] {
+    Graph& g = *G(h);
+    if (!sum_indeg_outdeg) fail(KCG_EINVAL, "null out pointer");
+    if (!g.has_rdag) {
+      if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
+      build_dag(g, false);
+    }
+    *sum_indeg_outdeg = dag_work(g);
+  });
+}
+
+int kcg_count_range(kcg_graph* h, int k, uint32_t r_lo, uint32_t r_hi, uint64_t* total,
+                    uint64_t* per_vertex) {
+  return count_range_impl(h, k, false, 0, 0, r_lo, r_hi, total, per_vertex);
+}
+
+int kcg_count_part(kcg_graph* h, int k, uint32_t part, uint32_t nparts, uint64_t* total,
+                   uint64_t* per_vertex) {
+  return count_range_impl(h, k, true, part, nparts, 0, 0, total, per_vertex);
 }
 
 void* kcg_stream(kcg_graph* h) {

@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
 // smask (rank space, optional): only sources r with smask[r] != 0 (the
 // peeling updates count the region around a batch, kcg_peel.cu).
 __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, uint32_t dmin,
-                                uint32_t part, uint32_t nparts,
+                                uint32_t r_lo, uint32_t r_hi,
                                 const uint8_t* __restrict__ smask,
                                 uint32_t* __restrict__ wlist, uint32_t* __restrict__ clist,
                                 uint32_t* __restrict__ ckey, unsigned* __restrict__ cnt) {
@@ -1010,7 +1010,7 @@ __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, ui
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const uint32_t r = base + threadIdx.x;
     uint32_t d = 0;
-    if (r < n && r % nparts == part && (!smask || smask[r])) d = uint32_t(off[r + 1] - off[r]);
+    if (r < n && r >= r_lo && r < r_hi && (!smask || smask[r])) d = uint32_t(off[r + 1] - off[r]);
     const bool inw = r < n && d >= dmin && d <= 32;
     const bool inc = r < n && d >= dmin && d > 32;
     unsigned bw = __ballot_sync(FULL, inw), bc = __ballot_sync(FULL, inc);
@@ -1034,12 +1034,12 @@ __global__ void classify_kernel(const uint64_t* __restrict__ off, uint32_t n, ui
 // a 2-clique; the total is summed on the device so that partial and
 // source-masked counts need no host pass over the offsets.
 __global__ void k2_kernel(const uint64_t* __restrict__ rdag_off,
-                          const uint32_t* __restrict__ rdag_adj, uint32_t n, uint32_t part,
-                          uint32_t nparts, const uint8_t* __restrict__ smask,
+                          const uint32_t* __restrict__ rdag_adj, uint32_t n, uint32_t r_lo,
+                          uint32_t r_hi, const uint8_t* __restrict__ smask,
                           ull* __restrict__ pv_rank, ull* __restrict__ total) {
   ull t = 0;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (r % nparts != part || (smask && !smask[r])) continue;
+    if (r < r_lo || r >= r_hi || (smask && !smask[r])) continue;
     const uint64_t b = rdag_off[r], e = rdag_off[r + 1];
     t += e - b;
     if (pv_rank) {
@@ -1049,6 +1049,52 @@ __global__ void k2_kernel(const uint64_t* __restrict__ rdag_off,
   }
   t = warp_sum(t);
   if ((threadIdx.x & 31) == 0 && t) atomicAdd(total, t);
+}
+
+// Work estimate of source r for the multi-GPU split:
+// w(r) = 1 + d + sum_{x in N+(r)} (1 + d+(x)) -- the staging reads of the
+// per-source scheme (the B_alg term 4 * sum indeg * outdeg, source by
+// source) -- plus d^2 for the k >= 5 edge searches.  One warp per source.
+__global__ void source_work_kernel(const uint64_t* __restrict__ off,
+                                   const uint32_t* __restrict__ adj, uint32_t n, int k,
+                                   ull* __restrict__ w) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t b = off[r], e = off[r + 1];
+    ull s = 0;
+    for (uint64_t p = b + lane; p < e; p += 32) {
+      const uint32_t x = adj[p];
+      s += 1 + (off[x + 1] - off[x]);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const ull d = e - b;
+      w[r] = 1 + d + s + (k >= 5 ? d * d : 0ull);
+    }
+  }
+}
+
+// bounds[p] = #{r : excl(r) * P < T * p}, excl = exclusive prefix of w,
+// T = its total; bounds[0] = 0, bounds[P] = n (shard.plan mirrors this)
+__global__ void plan_bounds_kernel(const ull* __restrict__ excl, const ull* __restrict__ w,
+                                   uint32_t n, uint32_t P, uint32_t* __restrict__ bounds) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > P) return;
+  if (p == 0 || n == 0) {
+    bounds[p] = p == 0 ? 0u : n;
+    return;
+  }
+  const unsigned __int128 T = (unsigned __int128)(excl[n - 1] + w[n - 1]) * p;
+  uint32_t lo = 0, hi = n;  // first r with excl(r) * P >= T * p
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if ((unsigned __int128)excl[mid] * P < T)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  bounds[p] = p == P ? n : lo;
 }
 
 __global__ void gather_pv_kernel(const ull* __restrict__ pv_rank, const uint32_t* __restrict__ rank,
@@ -1142,8 +1188,54 @@ inline ull* PVR(Graph& g) { return reinterpret_cast<ull*>(g.pv_rank.p); }
 
 }  // namespace
 
-uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t nparts) {
-  if (nparts == 0 || part >= nparts) fail(KCG_EINVAL, "part must be < nparts");
+void partition_plan(Graph& g, int k, uint32_t nparts, uint32_t* bounds) {
+  if (nparts == 0) fail(KCG_EINVAL, "nparts must be positive");
+  if (!g.has_rdag) fail(KCG_EINVAL, "no DAG on the handle");
+  const uint32_t n = g.n;
+  const size_t nb = (size_t(n) * 8 + 255) & ~size_t(255);
+  unsigned char* sb = g.scratch2.ensure(2 * nb + size_t(nparts + 1) * 4 + 1024, &g.alloc);
+  ull* w = reinterpret_cast<ull*>(sb);
+  ull* excl = reinterpret_cast<ull*>(sb + nb);
+  uint32_t* dbounds = reinterpret_cast<uint32_t*>(sb + 2 * nb);
+  if (n) {
+    source_work_kernel<<<blocks_for(uint64_t(n) * 32, 256), 256, 0, g.stream>>>(
+        g.rdag_off.p, g.rdag_adj.p, n, k, w);
+    KCG_LAUNCHED(g);
+    size_t tb = 0;
+    KCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, w, excl, n, g.stream));
+    KCG_CUDA(cub::DeviceScan::ExclusiveSum(cub_temp(g, tb), tb, w, excl, n, g.stream));
+  }
+  plan_bounds_kernel<<<(nparts + 1 + 127) / 128, 128, 0, g.stream>>>(excl, w, n, nparts,
+                                                                      dbounds);
+  KCG_LAUNCHED(g);
+  KCG_CUDA(cudaMemcpyAsync(bounds, dbounds, size_t(nparts + 1) * 4, cudaMemcpyDeviceToHost,
+                           g.stream));
+  g.sync();
+}
+
+uint64_t dag_work(Graph& g) {
+  if (!g.has_rdag) fail(KCG_EINVAL, "no DAG on the handle");
+  const uint32_t n = g.n;
+  if (n == 0) return 0;
+  const size_t nb = (size_t(n) * 8 + 255) & ~size_t(255);
+  unsigned char* sb = g.scratch2.ensure(nb + 256, &g.alloc);
+  ull* w = reinterpret_cast<ull*>(sb);
+  ull* sum = reinterpret_cast<ull*>(sb + nb);
+  source_work_kernel<<<blocks_for(uint64_t(n) * 32, 256), 256, 0, g.stream>>>(
+      g.rdag_off.p, g.rdag_adj.p, n, 4, w);
+  KCG_LAUNCHED(g);
+  size_t tb = 0;
+  KCG_CUDA(cub::DeviceReduce::Sum(nullptr, tb, w, sum, n, g.stream));
+  KCG_CUDA(cub::DeviceReduce::Sum(cub_temp(g, tb), tb, w, sum, n, g.stream));
+  ull h = 0;
+  KCG_CUDA(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, g.stream));
+  g.sync();
+  // sum_r w(r) = n + 2m + sum_w indeg(w) * outdeg(w)
+  return h - n - 2 * g.m;
+}
+
+uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_hi) {
+  if (r_lo > r_hi) fail(KCG_EINVAL, "source range must have r_lo <= r_hi");
   if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
   if (!g.has_rdag) fail(KCG_EINVAL, "no DAG on the handle");
   const uint32_t n = g.n;
@@ -1160,8 +1252,8 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
   if (k == 2) {
     g.mark(6);
     if (n) {
-      k2_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, n, part,
-                                                         nparts, g.src_mask,
+      k2_kernel<<<blocks_for(n, 256), 256, 0, g.stream>>>(g.rdag_off.p, g.rdag_adj.p, n, r_lo,
+                                                         r_hi, g.src_mask,
                                                          want_pv ? PVR(g) : nullptr, ctr);
       KCG_LAUNCHED(g);
     }
@@ -1178,7 +1270,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
     uint32_t* ckey2 = reinterpret_cast<uint32_t*>(sb + 4 * nb);
     unsigned* cnt = reinterpret_cast<unsigned*>(ctr + 2);
     classify_kernel<<<blocks_for(n, 256, 148u * 16u), 256, 0, g.stream>>>(
-        g.rdag_off.p, n, dmin, part, nparts, g.src_mask, wlist, clist, ckey, cnt);
+        g.rdag_off.p, n, dmin, r_lo, r_hi, g.src_mask, wlist, clist, ckey, cnt);
     KCG_LAUNCHED(g);
     unsigned hc[2] = {0, 0};
     KCG_CUDA(cudaMemcpyAsync(hc, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
@@ -1335,6 +1427,12 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part, uint32_t np
           arena = std::max<size_t>(arena, grid * per);
         }
       if (arena) g.heavy.ensure(arena, &g.alloc);
+      // the CTA launches read d_items and the heavy arena, which g.stream
+      // only just uploaded / allocated: re-fork after that work (a wait
+      // captures the event as recorded at call time, so re-recording the
+      // same event is safe; the warp tier above keeps running)
+      KCG_CUDA(cudaEventRecord(g.fork_ev, g.stream));
+      for (int i = 0; i < Graph::kAux; i++) KCG_CUDA(cudaStreamWaitEvent(g.aux[i], g.fork_ev, 0));
       for (const Plan& pl : plans) {
         a.item_src = d_items + first[pl.lo];
         a.item_sl = d_items + ni + first[pl.lo];

@@ -42,7 +42,10 @@ void set_last_error(const std::string& msg);
   } while (0)
 
 // ---- device buffers ----------------------------------------------------------
-// Stream-ordered allocations from the device's default memory pool (release
+// from the library's own pool (device().pool), else the default pool
+cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s);
+
+// Stream-ordered allocations from the library's memory pool (release
 // threshold raised at init), so creating and destroying handles -- the
 // end-to-end path of every drop-in call -- reuses memory instead of paying
 // cudaMalloc/cudaFree each time.
@@ -75,8 +78,8 @@ struct DevBuf {
     if (count <= n && p) return p;
     release();
     const size_t e = count ? count : 1;
-    KCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), e * sizeof(T),
-                             ctx ? ctx->stream : nullptr));
+    KCG_CUDA(alloc_async(reinterpret_cast<void**>(&p), e * sizeof(T),
+                         ctx ? ctx->stream : nullptr));
     n = e;
     if (ctx) ctx->bytes += n * sizeof(T);
     return p;
@@ -105,6 +108,7 @@ struct Device {
   int smem_optin = 227 * 1024;
   int l2 = 0;
   int major = 0, minor = 0;
+  cudaMemPool_t pool = nullptr;  // library-owned, release threshold raised
 };
 const Device& device();
 
@@ -178,8 +182,13 @@ uint64_t rank_graph(Graph& g, int strategy, double eps, uint64_t alpha_hat,
                     uint64_t* alpha_out);  // returns rounds
 void build_dag(Graph& g, bool want_id_dag);
 void relabel_from_dag(Graph& g);  // rdag from an adopted id-space DAG
-uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t part = 0,
-                       uint32_t nparts = 1);
+// cliques whose lowest-ranked vertex r lies in [r_lo, r_hi)
+uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo = 0,
+                       uint32_t r_hi = 0xffffffffu);
+// work-balanced contiguous source ranges (bounds[nparts + 1], rank space)
+void partition_plan(Graph& g, int k, uint32_t nparts, uint32_t* bounds);
+// sum_w indeg(w) * outdeg(w) of the DAG (the staging term of B_alg)
+uint64_t dag_work(Graph& g);
 
 // input construction on the device (kcg_build.cu)
 void build_from_edges(Graph& g, uint32_t n, const uint32_t* us, const uint32_t* vs,

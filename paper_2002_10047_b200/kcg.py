@@ -33,6 +33,7 @@ EXPORTED = [
     "kcg_num_edges", "kcg_rank", "kcg_estimate_arboricity", "kcg_set_ranking", "kcg_direct",
     "kcg_count", "kcg_per_vertex_device", "kcg_pipeline", "kcg_timings",
     "kcg_last_count_stats", "kcg_device_bytes", "kcg_synchronize", "kcg_count_part",
+    "kcg_count_range", "kcg_partition_plan", "kcg_dag_work",
     "kcg_stream", "kcg_update_counts", "kcg_peel_exact", "kcg_peel_approx",
     "kcg_graph_from_edges", "kcg_graph_rmat", "kcg_graph_csr", "kcg_colorful_sparsify",
     "kcg_approx_count", "kcg_list_cliques",
@@ -128,6 +129,9 @@ def lib():
         L.kcg_count.argtypes = [vp, ctypes.c_int, P(u64), vp]
         L.kcg_per_vertex_device.argtypes = [vp, P(vp)]
         L.kcg_count_part.argtypes = [vp, ctypes.c_int, u32, u32, P(u64), vp]
+        L.kcg_count_range.argtypes = [vp, ctypes.c_int, u32, u32, P(u64), vp]
+        L.kcg_partition_plan.argtypes = [vp, ctypes.c_int, u32, vp]
+        L.kcg_dag_work.argtypes = [vp, P(u64)]
         L.kcg_stream.argtypes = [vp]
         L.kcg_stream.restype = vp
         L.kcg_pipeline.argtypes = [vp, ctypes.c_int, ctypes.c_double, u64, ctypes.c_int,
@@ -303,12 +307,33 @@ class DeviceGraph:
         return int(total.value), (pv[:self.n] if per_vertex else None)
 
     def count_part(self, k: int, part: int, nparts: int, per_vertex=False):
-        """Cliques whose lowest-ranked vertex r has r % nparts == part."""
+        """Cliques whose lowest-ranked vertex lies in part `part` of
+        partition_plan(k, nparts)."""
         total = ctypes.c_uint64(0)
         pv = np.zeros(max(self.n, 1), np.uint64) if per_vertex else None
         _check(lib().kcg_count_part(self._h, int(k), int(part), int(nparts), ctypes.byref(total),
                                     pv.ctypes.data if per_vertex else None))
         return int(total.value), (pv[:self.n] if per_vertex else None)
+
+    def count_range(self, k: int, r_lo: int, r_hi: int, per_vertex=False):
+        """Cliques whose lowest-ranked vertex r has r_lo <= r < r_hi."""
+        total = ctypes.c_uint64(0)
+        pv = np.zeros(max(self.n, 1), np.uint64) if per_vertex else None
+        _check(lib().kcg_count_range(self._h, int(k), int(r_lo), int(r_hi), ctypes.byref(total),
+                                     pv.ctypes.data if per_vertex else None))
+        return int(total.value), (pv[:self.n] if per_vertex else None)
+
+    def dag_work(self) -> int:
+        """sum_w indeg(w) * outdeg(w) of the current DAG (device)."""
+        v = ctypes.c_uint64(0)
+        _check(lib().kcg_dag_work(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def partition_plan(self, k: int, nparts: int) -> np.ndarray:
+        """Work-balanced contiguous source ranges: nparts + 1 rank bounds."""
+        b = np.zeros(int(nparts) + 1, np.uint32)
+        _check(lib().kcg_partition_plan(self._h, int(k), int(nparts), b.ctypes.data))
+        return b
 
     def stream_ptr(self) -> int:
         return int(lib().kcg_stream(self._h) or 0)
