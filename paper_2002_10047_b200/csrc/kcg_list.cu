@@ -129,7 +129,6 @@ __global__ void range_mask_kernel(uint32_t n, uint32_t r0, uint32_t r1, uint8_t*
 
 uint64_t list_cliques(Graph& g, int k, uint64_t batch, kcg_clique_fn fn, void* user) {
   if (k < 2) fail(KCG_EINVAL, "k must be at least 2");
-  if (k > LIST_MAXK - 1) fail(KCG_EINVAL, "list_cliques supports k <= 33");
   if (!g.has_rdag) {
     if (!g.has_rank) fail(KCG_EINVAL, "no DAG: call kcg_rank/kcg_direct first");
     build_dag(g, false);
@@ -138,6 +137,12 @@ uint64_t list_cliques(Graph& g, int k, uint64_t batch, kcg_clique_fn fn, void* u
   const uint32_t n = g.n;
   const uint64_t total = count_cliques(g, k, false);
   if (total == 0 || n == 0) return total;
+  // any k is listed when there is nothing to list (the reference's
+  // recursion simply finds no clique); a graph that does hold a clique of
+  // 34+ vertices needs a deeper device stack than the listing kernel keeps
+  if (k > LIST_MAXK - 1)
+    fail(KCG_EINVAL, "list_cliques: the graph has " + std::to_string(total) + " " +
+                         std::to_string(k) + "-cliques; device listing supports k <= 33");
   // per-range clique counts with the source-masked counter
   DevBuf<uint8_t> mask;
   mask.ensure(n, &g.alloc);

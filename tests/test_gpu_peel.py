@@ -193,3 +193,22 @@ def test_peel_random_graphs_vs_port(port):
                 assert float(a["best_density"]).hex() == float(b["best_density"]).hex()
                 assert a["dense_vertices"].tolist() == b["dense_vertices"].tolist()
             assert ex["core"].tolist() == pex["core"].tolist()
+
+
+def test_update_counts_duplicate_batch_is_a_set():
+    """Documented difference: a batch with a repeated vertex
+    is treated as the set of its vertices -- the result equals the
+    de-duplicated batch's (the reference would charge the repeat twice,
+    peeling.cpp:143-174)."""
+    g = gen.gnp(40, 0.45, 31)
+    k = 4
+    with oriented(g) as h:
+        base, _ = h.count(k, per_vertex=True)
+        _, pv = h.count(k, per_vertex=True)
+        peeled = np.zeros(g.n, np.uint8)
+        c_set, c_dup = pv.copy(), pv.copy()
+        r_set = h.update_counts(k, c_set, [3, 7, 11], peeled)
+        r_dup = h.update_counts(k, c_dup, [7, 3, 7, 11, 3], peeled)
+    assert base > 0 and r_set[0] > 0
+    assert r_set[0] == r_dup[0] and r_set[1].tolist() == r_dup[1].tolist()
+    assert c_set.tolist() == c_dup.tolist()

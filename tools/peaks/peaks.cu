@@ -266,7 +266,7 @@ int main() {
     CK(cudaMemcpyFromSymbol(cyc.data(), g_cycles, sizeof(unsigned long long) * a.grid));
     const double cmax = double(*std::max_element(cyc.begin(), cyc.end()));
     const double mhz = cmax / (ms * 1e-3) / 1e6;
-    const double warp_inst = double(a.grid) * 32.0 * a.iters * 16 * 8;  // per op kind
+    const double warp_inst = double(a.grid) * (256 / 32) * a.iters * 16 * 8;  // per op kind
     const double per_sm_cycle = warp_inst / sms / (double(ms) * 1e-3 * mhz * 1e6);
     const double lane_ops = warp_inst * 32.0 / (ms * 1e-3);
     printf("%s\"%s\": {\"warp_inst_per_sm_cycle\": %.3f, \"lane_ops_per_s\": %.4g, \"sm_mhz\": %.0f, "
