@@ -5,7 +5,11 @@
 // else -> std::runtime_error.
 #pragma once
 
+#include <sys/mman.h>
+
+#include <cstdint>
 #include <new>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -13,6 +17,23 @@
 #include "kclique/graph.hpp"
 
 namespace kclique::b200 {
+
+// Sizes a large output vector with transparent huge pages requested for its
+// storage before the value-initialisation touches it (2 MB pages: 512x
+// fewer page faults when the vector is zero-filled and then pinned for the
+// device copy).  Small vectors are just resized.
+template <class T>
+void resize_huge(std::vector<T>& v, size_t n) {
+  const size_t bytes = n * sizeof(T);
+  if (bytes >= (size_t(4) << 20) && v.capacity() < n) {
+    v.reserve(n);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(v.data());
+    const uintptr_t lo = (a + (uintptr_t(2) << 20) - 1) & ~((uintptr_t(2) << 20) - 1);
+    const uintptr_t hi = (a + bytes) & ~((uintptr_t(2) << 20) - 1);
+    if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+  }
+  v.resize(n);
+}
 
 inline void check(int rc) {
   if (rc == KCG_OK) return;
@@ -29,8 +50,8 @@ struct GraphAccess {
     Graph g;
     g.n_ = kcg_num_vertices(h);
     g.m_ = kcg_num_edges(h);
-    g.offsets_.assign(size_t(g.n_) + 1, 0);
-    g.neighbors_.resize(2 * g.m_);
+    resize_huge(g.offsets_, size_t(g.n_) + 1);
+    resize_huge(g.neighbors_, 2 * g.m_);
     check(kcg_graph_csr(h, g.offsets_.data(), g.neighbors_.data()));
     return g;
   }

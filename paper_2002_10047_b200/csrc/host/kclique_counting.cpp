@@ -1,8 +1,10 @@
-// Drop-in counting entry points (include/kclique/counting.hpp): the
-// DirectedGraph is adopted by a device handle (kcg_dag_create, which
-// relabels it by rank on the GPU) and counted by kcg_count.
+// Drop-in counting entry points (include/kclique/counting.hpp): a
+// DirectedGraph from direct_by_ranking is counted on the handle that built
+// it; any other is adopted once by a device handle (kcg_dag_create, which
+// relabels it by rank on the GPU) and kept resident (kcg_cache.hpp).
 #include <exception>
 
+#include "kcg_cache.hpp"
 #include "kcg_handle.hpp"
 #include "kclique/counting.hpp"
 
@@ -16,10 +18,13 @@ CliqueCounts run(const DirectedGraph& dg, int k, bool per_vertex) {
   if (k < 2) throw std::invalid_argument("k must be at least 2");
   CliqueCounts out;
   out.k = k;
-  if (per_vertex) out.per_vertex.assign(dg.num_vertices(), 0);
+  if (per_vertex) b200::resize_huge(out.per_vertex, dg.num_vertices());
   if (dg.num_vertices() == 0) return out;
-  auto h = b200::Handle::adopt(dg);
-  b200::check(kcg_count(h.get(), k, &out.total, per_vertex ? out.per_vertex.data() : nullptr));
+  // the resident whose device DAG mirrors dg (direct_by_ranking's), else
+  // dg's arrays adopted once and kept for the next call
+  auto res = b200::resident_for_dag(dg);
+  std::lock_guard<std::mutex> lk(res->mu);
+  b200::check(kcg_count(res->h, k, &out.total, per_vertex ? out.per_vertex.data() : nullptr));
   return out;
 }
 
@@ -39,7 +44,8 @@ CliqueCounts list_cliques(const DirectedGraph& dg, int k, const CountConfig&,
   CliqueCounts out;
   out.k = k;
   if (dg.num_vertices() == 0) return out;
-  auto h = b200::Handle::adopt(dg);
+  auto res = b200::resident_for_dag(dg);
+  std::lock_guard<std::mutex> lk(res->mu);
   // cliques arrive in device batches; each is reported in ascending rank
   // (an exception from the callback aborts the listing and is rethrown)
   struct Ctx {
@@ -57,7 +63,7 @@ CliqueCounts list_cliques(const DirectedGraph& dg, int k, const CountConfig&,
     }
     return 0;
   };
-  const int rc = kcg_list_cliques(h.get(), k, 0, fn, &ctx, &out.total);
+  const int rc = kcg_list_cliques(res->h, k, 0, fn, &ctx, &out.total);
   if (ctx.err) std::rethrow_exception(ctx.err);
   b200::check(rc);
   return out;

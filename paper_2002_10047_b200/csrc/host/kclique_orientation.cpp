@@ -1,5 +1,8 @@
-// Drop-in ranking entry points (include/kclique/orientation.hpp): each one
-// uploads the graph and runs the peeling rounds on the B200 (kcg_rank).
+// Drop-in ranking entry points (include/kclique/orientation.hpp): the graph
+// stays resident on the B200 across calls (kcg_cache.hpp) and the peeling
+// rounds run there (kcg_rank); the returned Ranking is remembered as the
+// one installed, so direct_by_ranking(g, r) uploads nothing.
+#include "kcg_cache.hpp"
 #include "kcg_handle.hpp"
 #include "kclique/orientation.hpp"
 
@@ -8,19 +11,26 @@ namespace {
 
 Ranking run(const Graph& g, int strategy, double eps, uint64_t alpha_hat, uint64_t* rounds,
             uint64_t* alpha_out = nullptr) {
-  std::vector<VertexId> rank(g.num_vertices());
+  std::vector<VertexId> rank;
+  b200::resize_huge(rank, g.num_vertices());
   uint64_t r = 0, a = 0;
   if (g.num_vertices() == 0) {
     // keep the reference's argument checks for the empty graph
     if ((strategy == KCG_GOODRICH_PSZONA || strategy == KCG_BARENBOIM_ELKIN) && !(eps > 0))
       throw std::invalid_argument("epsilon must be positive");
-  } else {
-    auto h = b200::Handle::upload(g);
-    b200::check(kcg_rank(h.get(), strategy, eps, alpha_hat, rank.data(), &r, &a));
+    if (rounds) *rounds = r;
+    if (alpha_out) *alpha_out = a;
+    return Ranking(std::move(rank));
   }
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
+  b200::set_keys(*res, {}, {});
+  b200::check(kcg_rank(res->h, strategy, eps, alpha_hat, rank.data(), &r, &a));
   if (rounds) *rounds = r;
   if (alpha_out) *alpha_out = a;
-  return Ranking(std::move(rank));
+  Ranking out(std::move(rank));  // the buffer moves with the returned value
+  b200::set_keys(*res, b200::key_of(out), {});
+  return out;
 }
 
 }  // namespace
@@ -44,9 +54,10 @@ Ranking rank_barenboim_elkin(const Graph& g, double epsilon, uint64_t alpha_hat,
 uint64_t estimate_arboricity(const Graph& g, double epsilon) {
   if (!(epsilon > 0)) throw std::invalid_argument("epsilon must be positive");
   if (g.num_vertices() == 0) return 1;
-  auto h = b200::Handle::upload(g);
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
   uint64_t a = 0;
-  b200::check(kcg_estimate_arboricity(h.get(), epsilon, &a));
+  b200::check(kcg_estimate_arboricity(res->h, epsilon, &a));
   return a;
 }
 

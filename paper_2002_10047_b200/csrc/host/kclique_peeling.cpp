@@ -1,10 +1,12 @@
-// Drop-in peeling entry points (include/kclique/peeling.hpp).  The graph is
-// uploaded with its DirectedGraph's ranking; the DAG is rebuilt on the
-// device (direct_by_ranking is a function of the two, graph.cpp:94-114)
-// and the rounds run in kcg_peel.cu.  BucketQueue is host bookkeeping with
+// Drop-in peeling entry points (include/kclique/peeling.hpp).  The graph
+// stays resident (kcg_cache.hpp); when its device DAG is not already dg's,
+// dg's ranking is installed and the DAG rebuilt on the device
+// (direct_by_ranking is a function of the two, graph.cpp:94-114); the
+// rounds run in kcg_peel.cu.  BucketQueue is host bookkeeping with
 // the reference's observable behaviour (peeling.hpp:12-53).
 #include <stdexcept>
 
+#include "kcg_cache.hpp"
 #include "kcg_handle.hpp"
 #include "kclique/peeling.hpp"
 
@@ -38,14 +40,6 @@ void BucketQueue::update(VertexId v, uint64_t value) {
 
 namespace {
 
-b200::Handle upload_oriented(const Graph& g, const DirectedGraph& dg) {
-  if (dg.num_vertices() != g.num_vertices())
-    throw std::invalid_argument("DirectedGraph does not match the graph");
-  auto h = b200::Handle::upload(g);
-  b200::check(kcg_set_ranking(h.get(), dg.ranking().ranks().data(), g.num_vertices()));
-  return h;
-}
-
 PeelOutcome outcome(const kcg_peel_result& r, std::vector<VertexId> dense,
                     std::vector<uint64_t> core) {
   PeelOutcome o;
@@ -68,11 +62,13 @@ UpdateResult update_counts(const Graph& g, const DirectedGraph& dg, int k,
   const VertexId n = g.num_vertices();
   if (counts.size() < n || peeled.size() < n)
     throw std::invalid_argument("counts and peeled must cover every vertex");
-  auto h = upload_oriented(g, dg);
+  auto dev = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(dev->mu);
+  b200::ensure_oriented(*dev, g, dg);
   UpdateResult res;
   std::vector<VertexId> changed(n);
   uint64_t nch = 0;
-  b200::check(kcg_update_counts(h.get(), k, counts.data(), batch.data(), batch.size(),
+  b200::check(kcg_update_counts(dev->h, k, counts.data(), batch.data(), batch.size(),
                                 peeled.data(), &res.removed, changed.data(), &nch));
   changed.resize(nch);
   res.changed = std::move(changed);
@@ -83,11 +79,13 @@ PeelOutcome peel_exact(const Graph& g, const DirectedGraph& dg, int k) {
   if (k < 2) throw std::invalid_argument("k must be at least 2");
   const VertexId n = g.num_vertices();
   if (n == 0) return PeelOutcome{};
-  auto h = upload_oriented(g, dg);
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
+  b200::ensure_oriented(*res, g, dg);
   kcg_peel_result r{};
   std::vector<uint64_t> core(n);
   std::vector<VertexId> dense(n);
-  b200::check(kcg_peel_exact(h.get(), k, &r, core.data(), dense.data()));
+  b200::check(kcg_peel_exact(res->h, k, &r, core.data(), dense.data()));
   return outcome(r, std::move(dense), std::move(core));
 }
 
@@ -96,10 +94,12 @@ PeelOutcome peel_approx(const Graph& g, const DirectedGraph& dg, int k, double e
   if (epsilon <= 0) throw std::invalid_argument("epsilon must be positive");
   const VertexId n = g.num_vertices();
   if (n == 0) return PeelOutcome{};
-  auto h = upload_oriented(g, dg);
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
+  b200::ensure_oriented(*res, g, dg);
   kcg_peel_result r{};
   std::vector<VertexId> dense(n);
-  b200::check(kcg_peel_approx(h.get(), k, epsilon, &r, dense.data()));
+  b200::check(kcg_peel_approx(res->h, k, epsilon, &r, dense.data()));
   return outcome(r, std::move(dense), {});
 }
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <stdexcept>
 
+#include "kcg_cache.hpp"
 #include "kcg_handle.hpp"
 #include "kclique/sampling.hpp"
 
@@ -28,9 +29,10 @@ int strategy_code(OrientStrategy s) {
 Graph colorful_sparsify(const Graph& g, uint64_t colors, uint64_t seed) {
   if (colors < 1) throw std::invalid_argument("colors must be at least 1");
   if (colors == 1) return g;
-  auto h = b200::Handle::upload(g);
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
   kcg_graph* out = nullptr;
-  b200::check(kcg_colorful_sparsify(h.get(), colors, seed, &out));
+  b200::check(kcg_colorful_sparsify(res->h, colors, seed, &out));
   b200::Handle sub(out);
   return b200::GraphAccess::download(sub.get());
 }
@@ -41,9 +43,10 @@ SampleEstimate approx_count(const Graph& g, int k, uint64_t colors, uint64_t see
   if (colors < 1) throw std::invalid_argument("colors must be at least 1");
   if (ocfg.alpha_hat && *ocfg.alpha_hat < 1)
     throw std::invalid_argument("alpha_hat must be >= 1");
-  auto h = b200::Handle::upload(g);
+  auto res = b200::resident_for_graph(g);
+  std::lock_guard<std::mutex> lk(res->mu);
   kcg_sample_estimate e{};
-  b200::check(kcg_approx_count(h.get(), k, colors, seed, strategy_code(ocfg.strategy),
+  b200::check(kcg_approx_count(res->h, k, colors, seed, strategy_code(ocfg.strategy),
                                ocfg.epsilon, ocfg.alpha_hat ? *ocfg.alpha_hat : 0, &e));
   SampleEstimate est;
   est.k = e.k;

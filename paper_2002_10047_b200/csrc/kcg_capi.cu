@@ -2,6 +2,7 @@
 // transfers, status-code mapping.  The compute phases live in
 // kcg_rank.cu, kcg_direct.cu and kcg_count.cu.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -231,17 +232,56 @@ const Graph* G(const kcg_graph* h) {
   return reinterpret_cast<const Graph*>(h);
 }
 
-// Stream-ordered host -> device copy on the handle's stream (a pageable
-// source is staged by the driver before the call returns).
+// Large transfers between the device and PAGEABLE host memory (the drop-in
+// API's std::vectors) pin the host range for the duration of the copy
+// (cudaHostRegister) so that it runs as one direct DMA instead of the
+// driver's staged pageable path; memory the caller already pinned is used
+// as is.  KCG_REGISTER=0 keeps the plain pageable copy.
+bool register_host() {
+  static const bool on = [] {
+    const char* e = getenv("KCG_REGISTER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+constexpr size_t kRegisterMin = size_t(8) << 20;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes attr;
+  const bool pinned = cudaPointerGetAttributes(&attr, p) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  (void)cudaGetLastError();
+  return pinned;
+}
+
+void transfer(Graph& g, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  void* host = kind == cudaMemcpyHostToDevice ? const_cast<void*>(src) : dst;
+  if (bytes >= kRegisterMin && register_host() && !is_pinned(host)) {
+    const unsigned flags = kind == cudaMemcpyHostToDevice ? cudaHostRegisterReadOnly
+                                                          : cudaHostRegisterDefault;
+    if (cudaHostRegister(host, bytes, flags) == cudaSuccess) {
+      const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, g.stream);
+      const cudaError_t s = e == cudaSuccess ? cudaStreamSynchronize(g.stream) : e;
+      cudaHostUnregister(host);
+      KCG_CUDA(s);
+      return;
+    }
+    (void)cudaGetLastError();  // not registrable: the staged copy below
+  }
+  KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, g.stream));
+}
+
+// Stream-ordered host <-> device copies on the handle's stream (a pageable
+// source is staged or registered before the call returns).
 void upload(Graph& g, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
-  KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g.stream));
+  transfer(g, dst, src, bytes, cudaMemcpyHostToDevice);
   g.times.h2d_bytes += bytes;
 }
 
 void download(Graph& g, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
-  KCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g.stream));
+  transfer(g, dst, src, bytes, cudaMemcpyDeviceToHost);
   g.times.d2h_bytes += bytes;
 }
 

@@ -32,6 +32,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "kcg_internal.cuh"
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     count_warp_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                       const uint32_t* __restrict__ srcs, uint32_t nsrc, int k,
                       ull* __restrict__ total_out, ull* __restrict__ pv_rank,
-                      ull* __restrict__ staged_out) {
+                      ull* __restrict__ staged_out, int combine) {
   struct WarpSmem {
     ull table[64];
     ull rbase[32];
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
         }
       }
       my_staged += T;
-      Stager<PV> st{M, sym, 1, S.qy, S.qi, lane, 0};
+      Stager<PV> st{M, sym, 1, S.qy, S.qi, lane, 0, combine != 0};
       const Rows rl{S.P, S.rbase, S.rowid, nl};
       stage_long(rl, st, adj, 0, Ll);
       const Rows rs{S.P + nl + 1, S.rbase + nl, S.rowid + nl, ns};
@@ -254,6 +255,11 @@ struct Lvl {
 struct Layout {
   uint32_t dmax, wpmax, tbits, fbits, levels;
   uint32_t lean;  // k = 4 counts: rows padded to 4 words only, warp areas = queues
+                  // (tried this round: the bank-spread stride of row_stride, or
+                  // power-of-two groups with an XOR swizzle of the groups -- 21%
+                  // fewer shared wavefronts in the pair pass, but config 2 k=4
+                  // 12.97 -> 13.7 / 15.0 ms from the lost occupancy and the
+                  // extra address arithmetic)
   size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
   size_t sym_bytes;  // the bitmap; inside `total` unless sym_apart
   // per-warp offsets
@@ -681,6 +687,7 @@ struct CtaArgs {
   unsigned* work;        // work-item counter
   unsigned char* gbase;  // global working sets (heavy tier)
   Layout L;
+  int combine;           // Stager: pre-combine same-word hits
 };
 
 // GWS = false: the whole working set is dynamic shared memory (the
@@ -813,7 +820,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     // stage the induced subgraph: each warp one contiguous 1/NW of the
     // long-row elements and of the short-row elements
     {
-      Stager<PV> st{M, sym, wp, c.qy, c.qy + 64, lane, 0};
+      Stager<PV> st{M, sym, wp, c.qy, c.qy + 64, lane, 0, a.combine != 0};
       const Rows rl{rP, rbase, rowid, nl};
       stage_long(rl, st, a.adj, uint32_t(uint64_t(Ll) * wib / NW),
                  uint32_t(uint64_t(Ll) * (wib + 1) / NW));
@@ -1184,6 +1191,18 @@ inline uint32_t slices_for(uint32_t d, int k) {
   return std::min<uint32_t>(64, d / 64);
 }
 
+// Pre-combining of same-word staging hits (Stager::set): 2 = warp tier only
+// (default: its rows are single words, so a batch's hits collide; config 4
+// k=6 50.4 -> 46.4 ms, per-vertex 211.6 -> 182.3 ms), 1 = every tier
+// (config 2 k=4 12.97 -> 13.94 ms), 0 = off.  KCG_COMBINE overrides.
+inline int combine_mode() {
+  static const int m = [] {
+    const char* e = getenv("KCG_COMBINE");
+    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
+  return m;
+}
+
 inline ull* PVR(Graph& g) { return reinterpret_cast<ull*>(g.pv_rank.p); }
 
 }  // namespace
@@ -1315,7 +1334,8 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       auto run = [&](auto kern) {
         KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
         kern<<<grid, WARP_THREADS_BLOCK, dsm, aux_stream(false)>>>(g.rdag_off.p, g.rdag_adj.p, wlist, nw, k,
-                                                          ctr, PVR(g), ctr + 1);
+                                                          ctr, PVR(g), ctr + 1,
+                                                          combine_mode() != 0);
       };
       if (want_pv)
         k <= 4 ? run(count_warp_kernel<true, 0>)
@@ -1361,6 +1381,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       a.total = ctr;
       a.pv_rank = PVR(g);
       a.staged = ctr + 1;
+      a.combine = combine_mode() == 1;
       const size_t budget = size_t(8) << 30;
       const uint32_t levels = std::max<uint32_t>(R, 1);
       const bool big = k > 10;  // DFS engine stack depth 32 instead of 8

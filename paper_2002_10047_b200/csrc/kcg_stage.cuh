@@ -79,12 +79,27 @@ struct Stager {
   uint32_t* qi;  // 64 entries
   uint32_t lane;
   uint32_t qn;   // warp-uniform queue length
+  bool combine;  // pre-combine same-word hits before the atomic
 
-  __device__ __forceinline__ void set(uint32_t y, uint32_t i) {
-    const uint32_t j = member_probe(M, y);
-    if (j != NOTFOUND) {
-      atomicOr(&sym[i * wp + (j >> 5)], 1u << (j & 31));
-      if constexpr (SYM) atomicOr(&sym[j * wp + (i >> 5)], 1u << (i & 31));
+  // Called by all 32 lanes; `valid` lanes hold a queued candidate.  With
+  // `combine`, hits of one batch that land in the same bitmap word are
+  // OR-ed together first -- lanes grouped by address (MATCH), one REDUX.OR
+  // per group -- and only the group's first lane issues the atomic
+  // (same-word lanes of one ATOMS serialise on the bank).
+  __device__ __forceinline__ void set(uint32_t y, uint32_t i, bool valid) {
+    const uint32_t j = valid ? member_probe(M, y) : NOTFOUND;
+    const bool hit = j != NOTFOUND;
+    const uint32_t addr = hit ? i * wp + (j >> 5) : 0xffffffffu;
+    const uint32_t bits = hit ? 1u << (j & 31) : 0u;
+    if (combine) {
+      const unsigned mm = __match_any_sync(FULL, addr);
+      const uint32_t word = __reduce_or_sync(mm, bits);
+      if (hit && lane == uint32_t(__ffs(mm) - 1)) atomicOr(&sym[addr], word);
+    } else if (hit) {
+      atomicOr(&sym[addr], bits);
+    }
+    if constexpr (SYM) {
+      if (hit) atomicOr(&sym[j * wp + (i >> 5)], 1u << (i & 31));
     }
   }
   __device__ __forceinline__ void push(bool pass, uint32_t y, uint32_t row) {
@@ -110,13 +125,14 @@ struct Stager {
         qi[lane] = i1;
       }
       qn -= 32;
-      set(y0, i0);
+      set(y0, i0, true);
       __syncwarp();
     }
   }
   __device__ __forceinline__ void flush() {
     __syncwarp();
-    if (lane < qn) set(qy[lane], qi[lane]);
+    const bool v = lane < qn;
+    set(v ? qy[lane] : 0u, v ? qi[lane] : 0u, v);
     qn = 0;
     __syncwarp();
   }
