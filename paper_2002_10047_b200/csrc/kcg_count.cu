@@ -263,7 +263,7 @@ struct Layout {
   size_t sym, table, filter, rP, rbase, rowid, pvl, warp0, warp_stride;
   size_t sym_bytes;  // the bitmap; inside `total` unless sym_apart
   // per-warp offsets
-  size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk, w_q;
+  size_t w_cand, w_stack, w_csym, w_cusym, w_cpv, w_lvl, w_stk, w_q, w_fl;
   size_t total;
 };
 
@@ -299,10 +299,9 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   L.sym = at;
   L.sym_bytes = align_up(size_t(dmax) * L.wpmax * 4, 128);
   if (!sym_apart) at = align_up(at + size_t(dmax) * L.wpmax * 4, 16);
-  L.table = at;
-  at = align_up(at + (size_t(1) << tb) * 8, 16);
+  L.table = at;  // bucketed membership table (kcg_stage.cuh: Buckets)
+  at = align_up(at + bucket_bytes(dmax), 16);
   L.filter = at;
-  at = align_up(at + (size_t(1) << L.fbits) / 8, 16);
   L.rP = at;
   at = align_up(at + (size_t(dmax) + 2) * 4, 16);
   L.rbase = at;
@@ -313,9 +312,11 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   at = align_up(at + (pv ? size_t(dmax) * 8 : 0), 16);
   L.warp0 = at;
   size_t w = 0;
+  const size_t flb = align_up(size_t(32) * ((dmax + 31) / 32), 16);  // staging flag row
   if (lean) {
     L.w_cand = L.w_stack = L.w_csym = L.w_cusym = L.w_cpv = L.w_lvl = L.w_stk = L.w_q = 0;
-    L.warp_stride = 128 * 4;
+    L.w_fl = 0;
+    L.warp_stride = flb;
     L.total = align_up(at + L.warp_stride * nw, 128);
     return L;
   }
@@ -335,6 +336,8 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   w = align_up(w + stk_bytes, 16);
   L.w_q = w;
   w = align_up(w + 128 * 4, 16);
+  L.w_fl = w;
+  w = align_up(w + flb, 16);
   L.warp_stride = w;
   L.total = align_up(at + w * nw, 128);
   return L;
@@ -724,8 +727,6 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     base = smem;
     sym = reinterpret_cast<uint32_t*>(base + L.sym);
   }
-  ull* table = reinterpret_cast<ull*>(base + L.table);
-  uint32_t* filter = reinterpret_cast<uint32_t*>(base + L.filter);
   uint32_t* rP = reinterpret_cast<uint32_t*>(base + L.rP);
   ull* rbase = reinterpret_cast<ull*>(base + L.rbase);
   uint32_t* rowid = reinterpret_cast<uint32_t*>(base + L.rowid);
@@ -746,6 +747,10 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   c.lane = lane;
   const int R = a.k - 2;
   ull my_total = 0, my_staged = 0;
+  if constexpr (GWS == WS_SMEM) {  // staging flag row: zero between rows
+    uint32_t* fl = reinterpret_cast<uint32_t*>(wbase + L.w_fl);
+    for (uint32_t i = lane; i < 8 * ((L.dmax + 31) / 32); i += 32) fl[i] = 0;
+  }
   for (;;) {
     if (threadIdx.x == 0) {
       s_src = atomicAdd(a.work, 1u);
@@ -760,75 +765,59 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     const uint64_t b = a.off[u];
     const uint32_t d = uint32_t(a.off[u + 1] - b);
     const uint32_t W = (d + 31) / 32, wp = L.lean ? lean_stride(W) : row_stride(W);
-    uint32_t tb = 6;
-    while ((1u << tb) < 2 * d) tb++;
-    const uint32_t fb = tb + 4 > 14 ? (tb + 4 > 20 ? 20 : tb + 4) : 14;
-    const Member M{table, filter, tb, fb};
+    Buckets T = bucket_view(base + L.table, bucket_bits(d), bucket_bits(L.dmax));
     c.wp = wp;
     c.W = W;
     for (uint32_t i = threadIdx.x; i < d * wp; i += NT) sym[i] = 0;
-    for (uint32_t i = threadIdx.x; i < (1u << tb); i += NT) table[i] = EMPTY64;
-    for (uint32_t i = threadIdx.x; i < (1u << fb) / 32; i += NT) filter[i] = 0;
+    bucket_clear(T, threadIdx.x, NT);
     if constexpr (PV) {
       for (uint32_t i = threadIdx.x; i < d; i += NT) pvl[i] = 0;
     }
     __syncthreads();
-    // membership table + the non-empty rows with their prefix positions,
-    // long rows (>= 32 elements) first, then short ones (pass 1); one
-    // packed (rows << 40 | elements) block scan per NT rows
-    uint32_t nl = 0, Ll = 0, ns = 0, Ls = 0;
-    for (int pass = 0; pass < 2; pass++) {
-      uint32_t nr = 0, Lsum = 0;
-      uint32_t* P = pass ? rP + nl + 1 : rP;
-      ull* rb_out = pass ? rbase + nl : rbase;
-      uint32_t* id_out = pass ? rowid + nl : rowid;
-      for (uint32_t t0 = 0; t0 < d; t0 += NT) {
-        const uint32_t i = t0 + threadIdx.x;
-        uint32_t len = 0;
-        uint64_t rb = 0;
-        if (i < d) {
-          const uint32_t w = a.adj[b + i];
-          if (pass == 0) member_insert(M, w, i);
-          rb = a.off[w];
-          len = uint32_t(a.off[w + 1] - rb);
-          if (pass == 0 ? len < 32 : (len == 0 || len >= 32)) len = 0;
-        }
-        const ull v = (len ? (1ull << 40) : 0ull) | len;
-        ull excl, agg;
-        BlockScanU64(s_scan).ExclusiveSum(v, excl, agg);
-        if (len) {
-          const uint32_t ci = nr + uint32_t(excl >> 40);
-          P[ci] = Lsum + uint32_t(excl & ((1ull << 40) - 1));
-          rb_out[ci] = rb;
-          id_out[ci] = i;
-        }
-        nr += uint32_t(agg >> 40);
-        Lsum += uint32_t(agg & ((1ull << 40) - 1));
+    // membership table + the list of rows to scan: rows with out-neighbours
+    // (row d-1 holds no bits above its index: only the symmetric per-vertex
+    // bitmaps scan it); one packed (rows << 40 | elements) block scan per NT
+    // rows
+    uint32_t nr = 0, Lsum = 0;
+    const uint32_t last = d - 1;  // row d-1 has no bits above its index
+    for (uint32_t t0 = 0; t0 < d; t0 += NT) {
+      const uint32_t i = t0 + threadIdx.x;
+      uint32_t len = 0;
+      uint64_t rb = 0;
+      if (i < d) {
+        const uint32_t w = a.adj[b + i];
+        rb = a.off[w];
+        len = uint32_t(a.off[w + 1] - rb);
+        if (i >= last) len = 0;
+      }
+      const ull v = (len ? (1ull << 40) : 0ull) | len;
+      ull excl, agg;
+      BlockScanU64(s_scan).ExclusiveSum(v, excl, agg);
+      if (len) {
+        const uint32_t ci = nr + uint32_t(excl >> 40);
+        rP[ci] = len;
+        rbase[ci] = rb;
+        rowid[ci] = i;
+      }
+      nr += uint32_t(agg >> 40);
+      Lsum += uint32_t(agg & ((1ull << 40) - 1));
+      __syncthreads();
+    }
+    bucket_build(T, a.adj + b, d, threadIdx.x, NT);
+    if (threadIdx.x == 0) my_staged += Lsum;
+    // stage the induced subgraph: warps take whole rows
+    if constexpr (GWS == WS_SMEM) {
+      stage_rows(T, sym, wp, W, a.adj, rbase, rP, rowid, nr, &s_edge,
+                 reinterpret_cast<uint8_t*>(wbase + L.w_fl), lane);
+      if constexpr (PV) {
         __syncthreads();
+        mirror_lower(sym, wp, d, W, wib, NT / 32, lane);
       }
-      if (threadIdx.x == 0) P[nr] = Lsum;
-      if (pass == 0) {
-        nl = nr;
-        Ll = Lsum;
-      } else {
-        ns = nr;
-        Ls = Lsum;
-      }
+    } else {
+      stage_rows_atomic<PV>(T, sym, wp, a.adj, rbase, rP, rowid, nr, &s_edge, lane);
     }
-    if (threadIdx.x == 0) my_staged += Ll + Ls;
     __syncthreads();
-    // stage the induced subgraph: each warp one contiguous 1/NW of the
-    // long-row elements and of the short-row elements
-    {
-      Stager<PV> st{M, sym, wp, c.qy, c.qy + 64, lane, 0, a.combine != 0};
-      const Rows rl{rP, rbase, rowid, nl};
-      stage_long(rl, st, a.adj, uint32_t(uint64_t(Ll) * wib / NW),
-                 uint32_t(uint64_t(Ll) * (wib + 1) / NW));
-      const Rows rs{rP + nl + 1, rbase + nl, rowid + nl, ns};
-      stage_short(rs, st, a.adj, uint32_t(uint64_t(Ls) * wib / NW),
-                  uint32_t(uint64_t(Ls) * (wib + 1) / NW));
-      st.flush();
-    }
+    if (threadIdx.x == 0) s_edge = 0;
     __syncthreads();
     ull warp_src = 0;
     if (R == 2) {

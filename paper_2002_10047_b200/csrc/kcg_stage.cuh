@@ -236,3 +236,257 @@ __device__ __forceinline__ void stage_long(const Rows& R, ST& S,
 
 }  // namespace
 }  // namespace kcg
+
+namespace kcg {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Row-per-warp staging with a bucketed membership table (CTA / heavy tiers).
+//
+// The staging loop is bound by the integer ALU pipe and the shared-memory
+// crossbar (ncu: pipe_alu ~63 % of peak, lsu wavefronts next), so every
+// element costs as few ALU instructions and shared wavefronts as possible:
+//
+//  * N+(u) is hashed into B = 2^bb >= d+1 buckets of four u32 slots.  The
+//    hash h = y * mul (odd mul: a bijection of u32) names the bucket by its
+//    top bb bits; a slot stores h << bb (the other 32-bb bits of h) plus the
+//    local index (idx < d < B fits the low bb bits).  For a probe,
+//    slot - (h << bb) is the index when the slot holds y and >= B otherwise
+//    (mod 2^32), so one LDS.128, four subtractions and three unsigned
+//    minima give the index or a miss (empty slots are all ones and decode
+//    to B-1, the miss code).  The multiplier is chosen per source so that
+//    no bucket holds more than four keys (a few retries at most); only if
+//    eight multipliers fail does the source fall back to an overflow list
+//    (CTA-uniform flag, never taken on the benchmark graphs).
+//  * Warps take whole rows N+(w_i) from a shared counter (row i is then
+//    written by one warp only) and read them 128 elements per step.  A hit
+//    writes a byte flag at its local index in the warp's flag row (plain
+//    STS.U8, no atomics: distinct indices); when the row is done, one
+//    ballot per bitmap word turns the flags into row i's words and clears
+//    them.
+//
+// The reference's equivalent is the stamp test of counting.cpp:31-40.
+// ---------------------------------------------------------------------------
+constexpr uint32_t BKT_OVF_CAP = 64;
+constexpr uint32_t BKT_HASH = 0x9E3779B1u;
+constexpr uint32_t BKT_TRIES = 8;
+
+struct Buckets {
+  uint4* keys;      // B buckets x 4 slots (EMPTY = all ones)
+  uint32_t* cnt;    // B insert counts
+  uint32_t* flag;   // B bits: bucket overflowed (overflow mode)
+  uint2* ovf;       // (key, local index), BKT_OVF_CAP entries
+  uint32_t* ovf_n;  // overflow entries used
+  uint32_t bb;      // log2 B
+  uint32_t mul;     // hash multiplier (odd)
+  bool ovf_mode;    // CTA-uniform: some bucket holds more than four keys
+};
+
+// B = 2^bb >= d + 1 (index B-1 is the miss code), at least 32
+__host__ __device__ inline uint32_t bucket_bits(uint32_t d) {
+  uint32_t bb = 5;
+  while ((1u << bb) < d + 1) bb++;
+  return bb;
+}
+// bytes of a bucket table for sources of out-degree <= dmax
+__host__ __device__ inline size_t bucket_bytes(uint32_t dmax) {
+  const size_t B = size_t(1) << bucket_bits(dmax);
+  return B * 16 + B * 4 + B / 8 + BKT_OVF_CAP * 8 + 16;
+}
+__device__ __forceinline__ Buckets bucket_view(unsigned char* p, uint32_t bb, uint32_t bbmax) {
+  const size_t B = size_t(1) << bbmax;
+  Buckets T;
+  T.keys = reinterpret_cast<uint4*>(p);
+  T.cnt = reinterpret_cast<uint32_t*>(p + B * 16);
+  T.flag = reinterpret_cast<uint32_t*>(p + B * 20);
+  T.ovf = reinterpret_cast<uint2*>(p + B * 20 + B / 8);
+  T.ovf_n = reinterpret_cast<uint32_t*>(p + B * 20 + B / 8 + BKT_OVF_CAP * 8);
+  T.bb = bb;
+  T.mul = BKT_HASH;
+  T.ovf_mode = false;
+  return T;
+}
+// all threads of the CTA: EMPTY slots, zero counts and flags
+__device__ __forceinline__ void bucket_clear(const Buckets& T, uint32_t t, uint32_t nt) {
+  const uint32_t B = 1u << T.bb;
+  for (uint32_t b = t; b < B; b += nt) {
+    T.keys[b] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+    T.cnt[b] = 0;
+  }
+  for (uint32_t b = t; b < B / 32; b += nt) T.flag[b] = 0;
+  if (t == 0) *T.ovf_n = 0;
+}
+// Inserts key with local index i.  Returns false if its bucket already
+// holds four keys: in strict mode (ovf_mode off) the caller retries the
+// whole table with another multiplier; in overflow mode the key goes to the
+// overflow list (false only when that list is full too).
+__device__ __forceinline__ bool bucket_insert(const Buckets& T, uint32_t key, uint32_t i) {
+  const uint32_t h = key * T.mul;
+  const uint32_t b = h >> (32 - T.bb);
+  const uint32_t s = atomicAdd(&T.cnt[b], 1u);
+  if (s < 4) {
+    reinterpret_cast<uint32_t*>(T.keys)[4 * b + s] = (h << T.bb) | i;
+    return true;
+  }
+  if (!T.ovf_mode) return false;
+  atomicOr(&T.flag[b >> 5], 1u << (b & 31));
+  const uint32_t o = atomicAdd(T.ovf_n, 1u);
+  if (o >= BKT_OVF_CAP) return false;
+  T.ovf[o] = make_uint2(key, i);
+  return true;
+}
+// The local index of y, or B-1 (miss).  Warp-synchronous in overflow mode.
+__device__ __forceinline__ uint32_t bucket_find(const Buckets& T, uint32_t y, bool valid) {
+  const uint32_t B = 1u << T.bb;
+  const uint32_t h = y * T.mul;
+  const uint32_t b = h >> (32 - T.bb);
+  const uint32_t t = h << T.bb;
+  const uint4 q = T.keys[b];
+  uint32_t j = min(min(q.x - t, q.y - t), min(q.z - t, q.w - t));
+  j = valid ? min(j, B - 1) : B - 1;
+  if (T.ovf_mode) {
+    const bool full_miss = j == B - 1 && valid && q.w != EMPTY;
+    if (__any_sync(FULL, full_miss)) {
+      if (full_miss && ((T.flag[b >> 5] >> (b & 31)) & 1u)) {
+        const uint32_t no = min(*T.ovf_n, BKT_OVF_CAP);
+        for (uint32_t o = 0; o < no; o++) {
+          const uint2 e = T.ovf[o];
+          if (e.x == y) j = e.y;
+        }
+      }
+    }
+  }
+  return j;
+}
+
+// Builds the table for the d keys adj[0..d) (all threads of the CTA; ends
+// with a barrier).  Strict multipliers first, then overflow mode.
+__device__ __forceinline__ void bucket_build(Buckets& T, const uint32_t* __restrict__ keys,
+                                             uint32_t d, uint32_t t, uint32_t nt) {
+  for (uint32_t attempt = 0;; attempt++) {
+    if (attempt) {
+      T.mul = BKT_HASH + 2u * 0x632BE5ABu * attempt;
+      T.ovf_mode = attempt >= BKT_TRIES;
+      bucket_clear(T, t, nt);
+      __syncthreads();
+    }
+    bool ok = true;
+    for (uint32_t i = t; i < d; i += nt) ok &= bucket_insert(T, keys[i], i);
+    if (__syncthreads_and(ok)) return;
+  }
+}
+
+// Rows r in [0, nr): row rowid[r] = N+(w) at adj[rbase[r] ..+ rlen[r]),
+// written as bits above the diagonal (ascending local indices).  `fl` is
+// the warp's flag row (>= 32*W bytes, zero on entry and on exit).
+__device__ __forceinline__ void stage_rows(const Buckets& T, uint32_t* sym, uint32_t wp,
+                                           uint32_t W, const uint32_t* __restrict__ adj,
+                                           const ull* rbase, const uint32_t* rlen,
+                                           const uint32_t* rowid, uint32_t nr,
+                                           unsigned* row_ctr, uint8_t* fl, uint32_t lane) {
+  const uint32_t NF = (1u << T.bb) - 1;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(row_ctr, 1u);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= nr) break;
+    const uint32_t i = rowid[r], len = rlen[r];
+    const uint32_t* src = adj + rbase[r];
+    for (uint32_t p0 = 0; p0 < len; p0 += 32 * STAGE_U) {
+      uint32_t y[STAGE_U];
+#pragma unroll
+      for (int u = 0; u < STAGE_U; u++) {
+        const uint32_t p = p0 + 32 * u + lane;
+        y[u] = p < len ? __ldg(src + p) : EMPTY;
+      }
+#pragma unroll
+      for (int u = 0; u < STAGE_U; u++) {
+        const uint32_t j = bucket_find(T, y[u], p0 + 32 * u + lane < len);
+        if (j != NF) fl[j] = 1;
+      }
+    }
+    __syncwarp();
+    // flags -> words of row i (lowest possible hit: i + 1)
+    uint32_t* dst = sym + size_t(i) * wp;
+    for (uint32_t w = (i + 1) >> 5; w < W; w++) {
+      const uint32_t f = fl[32 * w + lane];
+      const uint32_t word = __ballot_sync(FULL, f != 0);
+      if (f) fl[32 * w + lane] = 0;
+      if (lane == 0) dst[w] = word;
+    }
+    __syncwarp();
+  }
+}
+
+// Heavy tier (d > 1024, the bitmap in global memory): the same row walk
+// with one atomic per hit (SYM: also the mirrored bit).
+template <bool SYM>
+__device__ __forceinline__ void stage_rows_atomic(const Buckets& T, uint32_t* sym, uint32_t wp,
+                                                  const uint32_t* __restrict__ adj,
+                                                  const ull* rbase, const uint32_t* rlen,
+                                                  const uint32_t* rowid, uint32_t nr,
+                                                  unsigned* row_ctr, uint32_t lane) {
+  const uint32_t NF = (1u << T.bb) - 1;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(row_ctr, 1u);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= nr) break;
+    const uint32_t i = rowid[r], len = rlen[r];
+    const uint32_t* src = adj + rbase[r];
+    uint32_t* dst = sym + size_t(i) * wp;
+    for (uint32_t p0 = 0; p0 < len; p0 += 32 * STAGE_U) {
+      uint32_t y[STAGE_U];
+#pragma unroll
+      for (int u = 0; u < STAGE_U; u++) {
+        const uint32_t p = p0 + 32 * u + lane;
+        y[u] = p < len ? __ldg(src + p) : EMPTY;
+      }
+#pragma unroll
+      for (int u = 0; u < STAGE_U; u++) {
+        const uint32_t j = bucket_find(T, y[u], p0 + 32 * u + lane < len);
+        if (j != NF) {
+          atomicOr(dst + (j >> 5), 1u << (j & 31));
+          if constexpr (SYM) atomicOr(sym + size_t(j) * wp + (i >> 5), 1u << (i & 31));
+        }
+      }
+    }
+  }
+}
+
+// Fills the lower triangle of a bitmap whose upper triangle is staged
+// (per-vertex paths read symmetric rows): 32x32 blocks (I, J), I <= J, are
+// transposed with 32 ballots by one warp each.
+__device__ __forceinline__ void mirror_lower(uint32_t* sym, uint32_t wp, uint32_t d, uint32_t W,
+                                             uint32_t warp, uint32_t nwarps, uint32_t lane) {
+  const uint32_t nblk = W * (W + 1) / 2;
+  for (uint32_t blk = warp; blk < nblk; blk += nwarps) {
+    // blk -> (I, J) with I <= J, row-major over the upper triangle
+    uint32_t I = 0, rem = blk;
+    while (rem >= W - I) {
+      rem -= W - I;
+      I++;
+    }
+    const uint32_t J = I + rem;
+    const uint32_t r = 32 * I + lane;
+    const uint32_t up = r < d ? sym[size_t(r) * wp + J] : 0u;
+    uint32_t mine = 0;
+#pragma unroll 8
+    for (uint32_t c = 0; c < 32; c++) {
+      const uint32_t bal = __ballot_sync(FULL, (up >> c) & 1u);
+      if (lane == c) mine = bal;
+    }
+    // lane c: row 32J + c, word I (its bits are the rows 32I + l with bit
+    // (32J + c) set)
+    const uint32_t rc = 32 * J + lane;
+    if (rc < d) {
+      if (I == J)
+        sym[size_t(rc) * wp + I] = up | mine;
+      else
+        sym[size_t(rc) * wp + I] = mine;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace kcg
