@@ -705,6 +705,9 @@ struct CtaArgs {
 // WS_GLOBAL -- everything in the global slice (sources too large for the
 // shared part).
 constexpr int WS_SMEM = 0, WS_SYM_GLOBAL = 1, WS_GLOBAL = 2;
+// WS_TILED: k = 4 totals of heavy sources (kcg_heavy.cuh) -- the bitmap in a
+// global slice, counted through shared-memory tiles
+constexpr int WS_TILED = 3;
 
 template <bool PV, int GWS, int NT, int MAXL, int MB>
 __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
@@ -990,6 +993,14 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   }
 }
 
+}  // namespace
+}  // namespace kcg
+
+#include "kcg_heavy.cuh"
+
+namespace kcg {
+namespace {
+
 // ---------------------------------------------------------------------------
 // Setup kernels
 // ---------------------------------------------------------------------------
@@ -1161,6 +1172,27 @@ void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaS
   }
 }
 
+// Tiled heavy launch (k = 4 totals): 512-thread CTAs, two per SM when the
+// shared-memory plan allows it.
+constexpr int HV_NT = 512;
+inline unsigned heavy_grid(const HeavyArgs& hv, uint32_t nitems) {
+  auto kern = count_heavy4_kernel<HV_NT, 2>;
+  KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(hv.smem_bytes)));
+  int occ = 0;
+  KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, HV_NT, hv.smem_bytes));
+  return unsigned(std::min<uint64_t>(nitems, uint64_t(device().sms) * std::max(occ, 1)));
+}
+void launch_heavy4(Graph& g, HeavyArgs hv, cudaStream_t st) {
+  const unsigned grid = heavy_grid(hv, hv.nitems);
+  if (size_t(grid) * hv.slice_words * 4 > g.heavy.n) fail(KCG_ERUNTIME, "heavy arena too small");
+  hv.gbase = reinterpret_cast<uint32_t*>(g.heavy.p);
+  KCG_CUDA(cudaMemsetAsync(hv.work, 0, 4, st));
+  count_heavy4_kernel<HV_NT, 2><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+  KCG_LAUNCHED(g);
+  g.stats.launches++;
+}
+
 template <bool PV, int MAXL>
 constexpr size_t stk_bytes() {
   return sizeof(Stacks<PV, MAXL>);
@@ -1188,6 +1220,15 @@ inline int combine_mode() {
   static const int m = [] {
     const char* e = getenv("KCG_COMBINE");
     return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
+  return m;
+}
+
+// KCG_TILED=0 sends heavy k = 4 sources down the older global-bitmap path
+inline bool tiled_mode() {
+  static const bool m = [] {
+    const char* e = getenv("KCG_TILED");
+    return !(e && e[0] == '0');
   }();
   return m;
 }
@@ -1382,6 +1423,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
         Layout L;
         int gws;  // WS_*
         int nt;
+        HeavyArgs hv;  // WS_TILED
       };
       std::vector<Plan> plans;
       const size_t smem_cap = size_t(dev.smem_optin) - 1024;
@@ -1390,16 +1432,30 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       auto global_plan = [&](uint32_t lo, uint32_t hi, uint32_t dmax) {
         Layout Ls = make_layout(dmax, levels, want_pv, 16, sbytes, true);
         if (Ls.total <= smem_cap)
-          plans.push_back({lo, hi, Ls, WS_SYM_GLOBAL, 512});
+          plans.push_back({lo, hi, Ls, WS_SYM_GLOBAL, 512, HeavyArgs{}});
         else
           plans.push_back({lo, hi, make_layout(dmax, levels, want_pv, 16, sbytes), WS_GLOBAL,
-                           512});
+                           512, HeavyArgs{}});
       };
       // heavy: d > SMEM_TIER_MAX
       uint32_t pos = 0;
       while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
       if (pos) {
-        global_plan(0, pos, deg_at(0));
+        if (k == 4 && !want_pv && tiled_mode()) {
+          // tiled kernel up to HV_DMAX in two bins (bucket table and tile
+          // sizes follow the bin's largest source); beyond that the old path
+          uint32_t p0 = 0;
+          while (p0 < pos && deg_at(p0) > HV_DMAX) p0++;
+          if (p0) global_plan(0, p0, deg_at(0));
+          uint32_t p1 = p0;
+          while (p1 < pos && deg_at(p1) > 2047) p1++;
+          if (p1 > p0)
+            plans.push_back({p0, p1, Layout{}, WS_TILED, HV_NT, heavy_plan(deg_at(p0), HV_NT / 32)});
+          if (pos > p1)
+            plans.push_back({p1, pos, Layout{}, WS_TILED, HV_NT, heavy_plan(deg_at(p1), HV_NT / 32)});
+        } else {
+          global_plan(0, pos, deg_at(0));
+        }
         g.stats.sources_heavy = pos;
       }
       // shared-memory bins, sqrt(2) apart so each bin's footprint (and
@@ -1419,7 +1475,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
         if (Lb.total > smem_cap)
           global_plan(pos, end, deg_at(pos));
         else
-          plans.push_back({pos, end, Lb, WS_SMEM, nt});
+          plans.push_back({pos, end, Lb, WS_SMEM, nt, HeavyArgs{}});
         g.stats.sources_cta += end - pos;
         pos = end;
       }
@@ -1427,7 +1483,10 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       // on aux[0])
       size_t arena = 0;
       for (const Plan& pl : plans)
-        if (pl.gws != WS_SMEM) {
+        if (pl.gws == WS_TILED) {
+          arena = std::max<size_t>(
+              arena, size_t(heavy_grid(pl.hv, first[pl.hi] - first[pl.lo])) * pl.hv.slice_words * 4);
+        } else if (pl.gws != WS_SMEM) {
           const size_t per = ws_global_bytes(pl.gws, pl.L);
           const uint64_t fit = std::max<uint64_t>(1, budget / per);
           // resident CTAs: <= 4 per SM at 512 threads (2 for all-global)
@@ -1444,6 +1503,18 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       KCG_CUDA(cudaEventRecord(g.fork_ev, g.stream));
       for (int i = 0; i < Graph::kAux; i++) KCG_CUDA(cudaStreamWaitEvent(g.aux[i], g.fork_ev, 0));
       for (const Plan& pl : plans) {
+        if (pl.gws == WS_TILED) {
+          HeavyArgs hv = pl.hv;
+          hv.off = g.rdag_off.p;
+          hv.adj = g.rdag_adj.p;
+          hv.item_src = d_items + first[pl.lo];
+          hv.nitems = first[pl.hi] - first[pl.lo];
+          hv.total = ctr;
+          hv.staged = ctr + 1;
+          hv.work = work + wslot++;
+          launch_heavy4(g, hv, aux_stream(true));
+          continue;
+        }
         a.item_src = d_items + first[pl.lo];
         a.item_sl = d_items + ni + first[pl.lo];
         a.nitems = first[pl.hi] - first[pl.lo];

@@ -1,0 +1,256 @@
+// k = 4 totals for heavy sources (1024 < d < 4096): included by kcg_count.cu.
+//
+// The induced bitmap of such a source (d rows of ceil(d/32) words, up to
+// 1.5 MB) does not fit one SM's shared memory, and distributed shared memory
+// is no answer on this part: a remote SM's shared memory delivers ~20
+// B/clk, less than the L2 does (~66 B/clk per SM, profiles/r02_peaks.json).
+// So the bitmap lives in a per-CTA slice of global memory (L2) and the
+// triangle count of the induced DAG,
+//     sum over induced edges (i, x) of |N+(i) ∩ N+(x)|      (counting.cpp:115-123,
+//                                                            clique_rec.hpp:49-60),
+// is tiled like a matrix product: column block X (128 columns = one 16-byte
+// quad per row) keeps the rows x of that block resident in shared memory
+// (quads from X's own on: rows hold only bits above their index, so nothing
+// left of the block can count), row blocks I <= X stream through a second
+// tile, and every (I, X) pair of tiles is read from L2 once instead of once
+// per induced edge (config 5: 8.1 TB of L2 traffic in round 1's heavy
+// launch, 3.97x the algorithmic bytes).
+//
+// Inside a pair of tiles a warp takes whole rows i: the members x of row i
+// inside block X are the bits of the row's first quad; they go through a
+// 64-entry (i, x) queue that persists across rows, so every dot-product
+// step runs on 32 edges: row i is a multicast load (a batch spans few
+// rows) and the rows x are consecutive members of one row, which the odd
+// quad stride spreads over the bank groups.
+//
+// Staging is the shared-memory tiers' (kcg_stage.cuh: bucketed membership
+// table, byte flags, ballots) with whole rows written to the slice --
+// coalesced, no atomics, no memset -- and the next row's descriptor
+// (target, offsets) loaded while the current row is probed.
+#pragma once
+
+namespace kcg {
+namespace {
+
+constexpr uint32_t HV_TB = 128;     // rows per tile = columns per quad
+constexpr uint32_t HV_DMAX = 4095;  // largest out-degree the tiled kernel takes
+
+struct HeavyArgs {
+  const uint64_t* off;
+  const uint32_t* adj;
+  const uint32_t* item_src;
+  uint32_t nitems;
+  ull* total;
+  ull* staged;
+  unsigned* work;
+  uint32_t* gbase;     // per-CTA bitmap slices
+  size_t slice_words;  // words per slice
+  uint32_t bbmax;      // bucket bits of the launch's largest source
+  uint32_t qs;         // tile row stride in quads (odd)
+  uint32_t flag_stride;  // bytes per warp flag row
+  uint32_t off_flags, off_tile_x, off_tile_i, off_queue;  // dynamic smem offsets
+  uint32_t smem_bytes;
+};
+
+// dynamic shared memory plan for sources of out-degree <= dmax, NW warps
+inline HeavyArgs heavy_plan(uint32_t dmax, int nw) {
+  HeavyArgs a{};
+  a.bbmax = bucket_bits(dmax);
+  const uint32_t W = (dmax + 31) / 32, Q = (W + 3) / 4;
+  a.qs = Q | 1u;
+  a.flag_stride = uint32_t(align_up(size_t(32) * W, 16));
+  a.slice_words = size_t(dmax) * 4 * Q;
+  // phase A: membership table + flag rows; phase B: two tiles + queues
+  const size_t tb = align_up(bucket_bytes(dmax), 16);
+  const size_t phase_a = tb + size_t(a.flag_stride) * nw;
+  const size_t tile = size_t(HV_TB) * a.qs * 16;
+  a.off_flags = uint32_t(tb);
+  a.off_tile_x = 0;
+  a.off_tile_i = uint32_t(tile);
+  a.off_queue = uint32_t(2 * tile);
+  const size_t phase_b = 2 * tile + size_t(nw) * 64 * 4;
+  a.smem_bytes = uint32_t(align_up(std::max(phase_a, phase_b), 128));
+  return a;
+}
+
+__device__ __forceinline__ uint32_t popc_and4(const uint4& a, const uint4& b) {
+  return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+}
+
+// rows [row0, row0 + nrows) of the slice, quads [q0, q0 + qt) -> tile rows
+// of stride qs quads (all threads of the CTA; no barrier)
+template <int NT>
+__device__ __forceinline__ void heavy_load_tile(uint4* tile, const uint32_t* sym, uint32_t wp,
+                                                uint32_t row0, uint32_t nrows, uint32_t q0,
+                                                uint32_t qt, uint32_t qs) {
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t rpp = qt >= 32 ? 1u : 32u / qt;  // rows per warp pass
+  const uint32_t sub = lane / qt, q = lane - sub * qt;
+  if (sub >= rpp) return;
+  for (uint32_t r = wib * rpp + sub; r < nrows; r += (NT / 32) * rpp) {
+    const uint4* src = reinterpret_cast<const uint4*>(sym + size_t(row0 + r) * wp) + q0;
+    for (uint32_t c = q; c < qt; c += 32) tile[r * qs + c] = __ldcg(src + c);
+  }
+}
+
+template <int NT, int MB>
+__global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned s_src, s_row;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t* sym = a.gbase + size_t(blockIdx.x) * a.slice_words;
+  uint8_t* fl = smem + a.off_flags + size_t(wib) * a.flag_stride;
+  uint4* tile_x = reinterpret_cast<uint4*>(smem + a.off_tile_x);
+  uint4* tile_i = reinterpret_cast<uint4*>(smem + a.off_tile_i);
+  uint32_t* queue = reinterpret_cast<uint32_t*>(smem + a.off_queue) + wib * 64;
+  const uint32_t qs = a.qs;
+  ull my_total = 0, my_staged = 0;
+  auto grab = [&]() {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(&s_row, 1u);
+    return __shfl_sync(FULL, r, 0);
+  };
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_src = atomicAdd(a.work, 1u);
+      s_row = 0;
+    }
+    __syncthreads();
+    const uint32_t si = s_src;
+    if (si >= a.nitems) break;
+    const uint32_t u = a.item_src[si];
+    const uint64_t b = a.off[u];
+    const uint32_t d = uint32_t(a.off[u + 1] - b);
+    const uint32_t W = (d + 31) / 32, Q = (W + 3) / 4, wp = 4 * Q;
+    Buckets T = bucket_view(smem, bucket_bits(d), a.bbmax);
+    bucket_clear(T, threadIdx.x, NT);
+    for (uint32_t i = 4 * lane; i < a.flag_stride; i += 128)
+      *reinterpret_cast<uint32_t*>(fl + i) = 0;  // the tiles of the last source lay here
+    __syncthreads();
+    bucket_build(T, a.adj + b, d, threadIdx.x, NT);
+    // ---- staging: warps take whole rows; row d-1 has nothing above it
+    {
+      const uint32_t NF = (1u << T.bb) - 1;
+      auto desc = [&](uint32_t r, uint64_t& rb, uint32_t& len) {
+        rb = 0;
+        len = 0;
+        if (r + 1 < d) {
+          const uint32_t w = __ldg(a.adj + b + r);
+          rb = __ldg(a.off + w);
+          len = uint32_t(__ldg(a.off + w + 1) - rb);
+        }
+      };
+      uint32_t r = grab();
+      uint64_t rb;
+      uint32_t len;
+      desc(r, rb, len);
+      while (r < d) {
+        const uint32_t rn = grab();
+        uint64_t rbn;
+        uint32_t lenn;
+        desc(rn, rbn, lenn);  // in flight while this row is probed
+        const uint32_t* src = a.adj + rb;
+        for (uint32_t p0 = 0; p0 < len; p0 += 32 * STAGE_U) {
+          uint32_t y[STAGE_U];
+#pragma unroll
+          for (int v = 0; v < STAGE_U; v++) {
+            const uint32_t p = p0 + 32 * v + lane;
+            y[v] = p < len ? __ldg(src + p) : EMPTY;
+          }
+#pragma unroll
+          for (int v = 0; v < STAGE_U; v++) {
+            const uint32_t j = bucket_find(T, y[v], p0 + 32 * v + lane < len);
+            if (j != NF) fl[j] = 1;
+          }
+        }
+        if (lane == 0) my_staged += len;
+        __syncwarp();
+        // flags -> the whole row (zero left of the diagonal), 32 words per store
+        const uint32_t w_lo = (r + 1) >> 5;
+        uint32_t* dst = sym + size_t(r) * wp;
+        for (uint32_t w0 = 0; w0 < wp; w0 += 32) {
+          uint32_t mine = 0;
+          const uint32_t wend = min(w0 + 32, W);
+          for (uint32_t w = max(w0, w_lo); w < wend && len; w++) {
+            const uint32_t f = fl[32 * w + lane];
+            const uint32_t word = __ballot_sync(FULL, f != 0);
+            if (f) fl[32 * w + lane] = 0;
+            if (lane == (w & 31)) mine = word;
+          }
+          if (w0 + lane < wp) dst[w0 + lane] = mine;
+        }
+        __syncwarp();
+        r = rn;
+        rb = rbn;
+        len = lenn;
+      }
+    }
+    __syncthreads();  // the slice's rows are visible to the whole CTA
+    // ---- tiled triangle count of the induced DAG
+    ull acc = 0;
+    uint32_t qn = 0;  // (i, x) queue length, warp-uniform
+    for (uint32_t bx = 0; bx < Q; bx++) {
+      const uint32_t qt = Q - bx;
+      const uint32_t nx = min(HV_TB, d - HV_TB * bx);
+      heavy_load_tile<NT>(tile_x, sym, wp, HV_TB * bx, nx, bx, qt, qs);
+      // the diagonal pair first: it needs no second tile
+      for (uint32_t bi = bx + 1; bi-- > 0;) {
+        const uint4* ti = tile_x;
+        uint32_t ni = nx;
+        if (bi < bx) {
+          heavy_load_tile<NT>(tile_i, sym, wp, HV_TB * bi, HV_TB, bx, qt, qs);
+          ti = tile_i;
+          ni = HV_TB;
+        }
+        if (threadIdx.x == 0) s_row = 0;
+        __syncthreads();
+        auto run_batch = [&](bool valid) {
+          const uint32_t e = valid ? queue[lane] : 0u;
+          const uint4* pi = ti + (e >> 8) * qs;
+          const uint4* px = tile_x + (e & 255u) * qs;
+          uint32_t c = 0;
+          for (uint32_t q = 0; q < qt; q++) c += popc_and4(pi[q], px[q]);
+          acc += valid ? c : 0u;
+        };
+        for (;;) {
+          const uint32_t r = grab();
+          if (r >= ni) break;
+          const uint4 m4 = ti[r * qs];
+          const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const uint32_t v = mw[j];
+            if (v == 0) continue;
+            if ((v >> lane) & 1u) queue[qn + __popc(v & lt)] = (r << 8) | (32u * j + lane);
+            qn += __popc(v);
+            if (qn >= 32) {
+              __syncwarp();
+              const bool mv = lane + 32 < qn;
+              const uint32_t e1 = mv ? queue[lane + 32] : 0u;
+              run_batch(true);
+              __syncwarp();
+              if (mv) queue[lane] = e1;
+              qn -= 32;
+              __syncwarp();
+            }
+          }
+        }
+        // entries name rows of this pair of tiles: drain before they change
+        __syncwarp();
+        if (qn) run_batch(lane < qn);
+        qn = 0;
+        __syncthreads();
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) my_total += acc;
+  }
+  if (lane == 0) {
+    if (my_total) atomicAdd(a.total, my_total);
+    if (my_staged) atomicAdd(a.staged, my_staged);
+  }
+}
+
+}  // namespace
+}  // namespace kcg
