@@ -312,7 +312,7 @@ __host__ __device__ inline Layout make_layout(uint32_t dmax, uint32_t levels, bo
   at = align_up(at + (pv ? size_t(dmax) * 8 : 0), 16);
   L.warp0 = at;
   size_t w = 0;
-  const size_t flb = align_up(size_t(32) * ((dmax + 31) / 32), 16);  // staging flag row
+  const size_t flb = flag_row_bytes((dmax + 31) / 32);  // staging flag row
   if (lean) {
     L.w_cand = L.w_stack = L.w_csym = L.w_cusym = L.w_cpv = L.w_lvl = L.w_stk = L.w_q = 0;
     L.w_fl = 0;
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   ull my_total = 0, my_staged = 0;
   if constexpr (GWS == WS_SMEM) {  // staging flag row: zero between rows
     uint32_t* fl = reinterpret_cast<uint32_t*>(wbase + L.w_fl);
-    for (uint32_t i = lane; i < 8 * ((L.dmax + 31) / 32); i += 32) fl[i] = 0;
+    for (uint32_t i = lane; i < flag_row_bytes((L.dmax + 31) / 32) / 4; i += 32) fl[i] = 0;
   }
   for (;;) {
     if (threadIdx.x == 0) {
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
       Lsum += uint32_t(agg & ((1ull << 40) - 1));
       __syncthreads();
     }
-    bucket_build(T, a.adj + b, d, threadIdx.x, NT);
+    bucket_build<GWS == WS_SMEM>(T, a.adj + b, d, threadIdx.x, NT);
     if (threadIdx.x == 0) my_staged += Lsum;
     // stage the induced subgraph: warps take whole rows
     if constexpr (GWS == WS_SMEM) {

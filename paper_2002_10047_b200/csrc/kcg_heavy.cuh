@@ -58,7 +58,7 @@ inline HeavyArgs heavy_plan(uint32_t dmax, int nw) {
   a.bbmax = bucket_bits(dmax);
   const uint32_t W = (dmax + 31) / 32, Q = (W + 3) / 4;
   a.qs = Q | 1u;
-  a.flag_stride = uint32_t(align_up(size_t(32) * W, 16));
+  a.flag_stride = uint32_t(flag_row_bytes(W));
   a.slice_words = size_t(dmax) * 4 * Q;
   // phase A: membership table + flag rows; phase B: two tiles + queues
   const size_t tb = align_up(bucket_bytes(dmax), 16);
@@ -128,63 +128,51 @@ __global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
     for (uint32_t i = 4 * lane; i < a.flag_stride; i += 128)
       *reinterpret_cast<uint32_t*>(fl + i) = 0;  // the tiles of the last source lay here
     __syncthreads();
-    bucket_build(T, a.adj + b, d, threadIdx.x, NT);
+    bucket_build<true>(T, a.adj + b, d, threadIdx.x, NT);
     // ---- staging: warps take whole rows; row d-1 has nothing above it
     {
-      const uint32_t NF = (1u << T.bb) - 1;
-      auto desc = [&](uint32_t r, uint64_t& rb, uint32_t& len) {
-        rb = 0;
-        len = 0;
+      uint32_t* fl32 = reinterpret_cast<uint32_t*>(fl);
+      // the descriptor loads of a row are in flight while the row before it
+      // is probed (stage_scan asks one row ahead)
+      auto next = [&](StageRow& row) {
+        const uint32_t r = grab();
+        if (r >= d) return false;
+        row.i = r;
+        row.len = 0;
+        row.src = a.adj;
         if (r + 1 < d) {
           const uint32_t w = __ldg(a.adj + b + r);
-          rb = __ldg(a.off + w);
-          len = uint32_t(__ldg(a.off + w + 1) - rb);
+          const uint64_t rb = __ldg(a.off + w);
+          row.len = uint32_t(__ldg(a.off + w + 1) - rb);
+          row.src = a.adj + rb;
         }
+        return true;
       };
-      uint32_t r = grab();
-      uint64_t rb;
-      uint32_t len;
-      desc(r, rb, len);
-      while (r < d) {
-        const uint32_t rn = grab();
-        uint64_t rbn;
-        uint32_t lenn;
-        desc(rn, rbn, lenn);  // in flight while this row is probed
-        const uint32_t* src = a.adj + rb;
-        for (uint32_t p0 = 0; p0 < len; p0 += 32 * STAGE_U) {
-          uint32_t y[STAGE_U];
-#pragma unroll
-          for (int v = 0; v < STAGE_U; v++) {
-            const uint32_t p = p0 + 32 * v + lane;
-            y[v] = p < len ? __ldg(src + p) : EMPTY;
-          }
-#pragma unroll
-          for (int v = 0; v < STAGE_U; v++) {
-            const uint32_t j = bucket_find(T, y[v], p0 + 32 * v + lane < len);
-            if (j != NF) fl[j] = 1;
-          }
-        }
-        if (lane == 0) my_staged += len;
-        __syncwarp();
-        // flags -> the whole row (zero left of the diagonal), 32 words per store
-        const uint32_t w_lo = (r + 1) >> 5;
-        uint32_t* dst = sym + size_t(r) * wp;
+      // flags -> the whole row (zero left of the diagonal), 32 words per store
+      auto emit = [&](const StageRow& row) {
+        if (lane == 0) my_staged += row.len;
+        const uint32_t g_lo = (row.i + 1) >> 7;
+        uint32_t* dst = sym + size_t(row.i) * wp;
         for (uint32_t w0 = 0; w0 < wp; w0 += 32) {
           uint32_t mine = 0;
-          const uint32_t wend = min(w0 + 32, W);
-          for (uint32_t w = max(w0, w_lo); w < wend && len; w++) {
-            const uint32_t f = fl[32 * w + lane];
-            const uint32_t word = __ballot_sync(FULL, f != 0);
-            if (f) fl[32 * w + lane] = 0;
-            if (lane == (w & 31)) mine = word;
+          const uint32_t gend = min(w0 / 4 + 8, Q);
+          for (uint32_t g = max(w0 / 4, g_lo); g < gend && row.len; g++) {
+            const uint32_t x = fl32[32 * g + lane];
+            if (x) fl32[32 * g + lane] = 0;
+            const uint32_t b0 = __ballot_sync(FULL, x & 0x000000ffu);
+            const uint32_t b1 = __ballot_sync(FULL, x & 0x0000ff00u);
+            const uint32_t b2 = __ballot_sync(FULL, x & 0x00ff0000u);
+            const uint32_t b3 = __ballot_sync(FULL, x & 0xff000000u);
+            const uint32_t k = lane - ((4 * g) & 31u);
+            if (k < 4) mine = k == 0 ? b0 : k == 1 ? b1 : k == 2 ? b2 : b3;
           }
           if (w0 + lane < wp) dst[w0 + lane] = mine;
         }
-        __syncwarp();
-        r = rn;
-        rb = rbn;
-        len = lenn;
-      }
+      };
+      if (T.ovf_mode)
+        stage_scan<true>(T, fl, lane, next, emit);
+      else
+        stage_scan<false>(T, fl, lane, next, emit);
     }
     __syncthreads();  // the slice's rows are visible to the whole CTA
     // ---- tiled triangle count of the induced DAG

@@ -282,9 +282,20 @@ struct Buckets {
   bool ovf_mode;    // CTA-uniform: some bucket holds more than four keys
 };
 
-// B = 2^bb >= d + 1 (index B-1 is the miss code), at least 32
+// Flag byte of local index j in a warp's flag row: groups of 128 indices,
+// lane-major inside a group (index 128g + 32k + l is byte k of u32 32g + l),
+// so one LDS.32 per lane and four ballots give the group's four bitmap words.
+// A bijection of [0, B) for B >= 128 with flag_pos(B-1) = B-1, so positions
+// fit the table's index field and never equal the miss code.
+__host__ __device__ inline uint32_t flag_pos(uint32_t j) {
+  return (j & ~127u) | ((j & 31u) << 2) | ((j >> 5) & 3u);
+}
+// bytes of a flag row for bitmap rows of W words
+__host__ __device__ inline size_t flag_row_bytes(uint32_t W) { return size_t(128) * ((W + 3) / 4); }
+
+// B = 2^bb >= d + 1 (index B-1 is the miss code), at least 128 (flag_pos)
 __host__ __device__ inline uint32_t bucket_bits(uint32_t d) {
-  uint32_t bb = 5;
+  uint32_t bb = 7;
   while ((1u << bb) < d + 1) bb++;
   return bb;
 }
@@ -359,8 +370,36 @@ __device__ __forceinline__ uint32_t bucket_find(const Buckets& T, uint32_t y, bo
   return j;
 }
 
+// The stored index of y, or a value >= B-1 (miss); y = EMPTY always misses
+// (the hash is a bijection and EMPTY is no vertex id).  Warp-synchronous in
+// overflow mode.
+template <bool OVF>
+__device__ __forceinline__ uint32_t bucket_probe(const Buckets& T, uint32_t y) {
+  const uint32_t h = y * T.mul;
+  const uint32_t b = h >> (32 - T.bb);
+  const uint32_t t = h << T.bb;
+  const uint4 q = T.keys[b];
+  uint32_t j = min(min(q.x - t, q.y - t), min(q.z - t, q.w - t));
+  if constexpr (OVF) {
+    const uint32_t B = 1u << T.bb;
+    const bool full_miss = j >= B - 1 && y != EMPTY && q.w != EMPTY;
+    if (__any_sync(FULL, full_miss)) {
+      if (full_miss && ((T.flag[b >> 5] >> (b & 31)) & 1u)) {
+        const uint32_t no = min(*T.ovf_n, BKT_OVF_CAP);
+        for (uint32_t o = 0; o < no; o++) {
+          const uint2 e = T.ovf[o];
+          if (e.x == y) j = e.y;
+        }
+      }
+    }
+  }
+  return j;
+}
+
 // Builds the table for the d keys adj[0..d) (all threads of the CTA; ends
 // with a barrier).  Strict multipliers first, then overflow mode.
+// FLAGPOS: the stored index of key i is flag_pos(i) (stage_scan's tables).
+template <bool FLAGPOS = false>
 __device__ __forceinline__ void bucket_build(Buckets& T, const uint32_t* __restrict__ keys,
                                              uint32_t d, uint32_t t, uint32_t nt) {
   for (uint32_t attempt = 0;; attempt++) {
@@ -371,51 +410,120 @@ __device__ __forceinline__ void bucket_build(Buckets& T, const uint32_t* __restr
       __syncthreads();
     }
     bool ok = true;
-    for (uint32_t i = t; i < d; i += nt) ok &= bucket_insert(T, keys[i], i);
+    for (uint32_t i = t; i < d; i += nt)
+      ok &= bucket_insert(T, keys[i], FLAGPOS ? flag_pos(i) : i);
     if (__syncthreads_and(ok)) return;
+  }
+}
+
+// 128 entries (or the `rem` < 128 left, EMPTY beyond) at s -> z
+__device__ __forceinline__ void stage_load(const uint32_t* __restrict__ s, uint32_t rem,
+                                           uint32_t lane, uint32_t (&z)[STAGE_U]) {
+  static_assert(STAGE_U == 4, "chunk = 128 entries");
+  if (rem >= 128) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) z[v] = __ldg(s + 32 * v + lane);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; v++) z[v] = 32 * v + lane < rem ? __ldg(s + 32 * v + lane) : EMPTY;
+  }
+}
+
+struct StageRow {
+  uint32_t i, len;      // bitmap row and |N+(w_i)|
+  const uint32_t* src;  // N+(w_i)
+};
+
+// The scan of a warp's rows.  next(row) hands out the warp's next row (false:
+// none left); emit(row) turns the warp's flag row into bitmap words and
+// clears it.  Tables built with flag positions as indices (bucket_build<true>).
+// The 128 entries after the ones being probed -- the row's next chunk, or the
+// next row's first -- are always in flight.  EMPTY is no vertex id, so the
+// padding of a partial chunk never hits.
+template <bool OVF, class Next, class Emit>
+__device__ __forceinline__ void stage_scan(const Buckets& T, uint8_t* fl, uint32_t lane, Next next,
+                                           Emit emit) {
+  const uint32_t NF = (1u << T.bb) - 1;
+  auto probe = [&](uint32_t y) {
+    const uint32_t j = bucket_probe<OVF>(T, y);
+    if (j < NF) fl[j] = 1;
+  };
+  StageRow cur{0, 0, nullptr}, nxt{0, 0, nullptr};
+  uint32_t y[STAGE_U];
+  if (!next(cur)) return;
+  stage_load(cur.src, cur.len, lane, y);
+  for (;;) {
+    const bool have_next = next(nxt);
+    if (!have_next) nxt.len = 0;
+    const uint32_t* s = cur.src;
+    uint32_t rem = cur.len;
+    for (;;) {
+      const bool more = rem > 128;
+      uint32_t yn[STAGE_U];
+      stage_load(more ? s + 128 : nxt.src, more ? rem - 128 : nxt.len, lane, yn);
+      probe(y[0]);
+      if (rem > 32) probe(y[1]);
+      if (rem > 64) probe(y[2]);
+      if (rem > 96) probe(y[3]);
+#pragma unroll
+      for (int v = 0; v < STAGE_U; v++) y[v] = yn[v];
+      if (!more) break;
+      s += 128;
+      rem -= 128;
+    }
+    __syncwarp();
+    emit(cur);
+    __syncwarp();
+    if (!have_next) return;
+    cur = nxt;
   }
 }
 
 // Rows r in [0, nr): row rowid[r] = N+(w) at adj[rbase[r] ..+ rlen[r]),
 // written as bits above the diagonal (ascending local indices).  `fl` is
-// the warp's flag row (>= 32*W bytes, zero on entry and on exit).
+// the warp's flag row (flag_row_bytes(W), zero on entry and on exit).
+template <bool OVF>
+__device__ __forceinline__ void stage_rows_t(const Buckets& T, uint32_t* sym, uint32_t wp,
+                                             uint32_t W, const uint32_t* __restrict__ adj,
+                                             const ull* rbase, const uint32_t* rlen,
+                                             const uint32_t* rowid, uint32_t nr,
+                                             unsigned* row_ctr, uint8_t* fl, uint32_t lane) {
+  uint32_t* fl32 = reinterpret_cast<uint32_t*>(fl);
+  const uint32_t G = (W + 3) >> 2;
+  auto next = [&](StageRow& row) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(row_ctr, 1u);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= nr) return false;
+    row.i = rowid[r];
+    row.len = rlen[r];
+    row.src = adj + rbase[r];
+    return true;
+  };
+  // flags -> words of row i, four per step (lowest possible hit: i + 1)
+  auto emit = [&](const StageRow& row) {
+    uint32_t* dst = sym + size_t(row.i) * wp;
+    for (uint32_t g = (row.i + 1) >> 7; g < G; g++) {
+      const uint32_t x = fl32[32 * g + lane];
+      if (x) fl32[32 * g + lane] = 0;
+      const uint32_t b0 = __ballot_sync(FULL, x & 0x000000ffu);
+      const uint32_t b1 = __ballot_sync(FULL, x & 0x0000ff00u);
+      const uint32_t b2 = __ballot_sync(FULL, x & 0x00ff0000u);
+      const uint32_t b3 = __ballot_sync(FULL, x & 0xff000000u);
+      if (lane < 4) dst[4 * g + lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
+    }
+  };
+  stage_scan<OVF>(T, fl, lane, next, emit);
+}
 __device__ __forceinline__ void stage_rows(const Buckets& T, uint32_t* sym, uint32_t wp,
                                            uint32_t W, const uint32_t* __restrict__ adj,
                                            const ull* rbase, const uint32_t* rlen,
                                            const uint32_t* rowid, uint32_t nr,
                                            unsigned* row_ctr, uint8_t* fl, uint32_t lane) {
-  const uint32_t NF = (1u << T.bb) - 1;
-  for (;;) {
-    uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(row_ctr, 1u);
-    r = __shfl_sync(FULL, r, 0);
-    if (r >= nr) break;
-    const uint32_t i = rowid[r], len = rlen[r];
-    const uint32_t* src = adj + rbase[r];
-    for (uint32_t p0 = 0; p0 < len; p0 += 32 * STAGE_U) {
-      uint32_t y[STAGE_U];
-#pragma unroll
-      for (int u = 0; u < STAGE_U; u++) {
-        const uint32_t p = p0 + 32 * u + lane;
-        y[u] = p < len ? __ldg(src + p) : EMPTY;
-      }
-#pragma unroll
-      for (int u = 0; u < STAGE_U; u++) {
-        const uint32_t j = bucket_find(T, y[u], p0 + 32 * u + lane < len);
-        if (j != NF) fl[j] = 1;
-      }
-    }
-    __syncwarp();
-    // flags -> words of row i (lowest possible hit: i + 1)
-    uint32_t* dst = sym + size_t(i) * wp;
-    for (uint32_t w = (i + 1) >> 5; w < W; w++) {
-      const uint32_t f = fl[32 * w + lane];
-      const uint32_t word = __ballot_sync(FULL, f != 0);
-      if (f) fl[32 * w + lane] = 0;
-      if (lane == 0) dst[w] = word;
-    }
-    __syncwarp();
-  }
+  if (T.ovf_mode)
+    stage_rows_t<true>(T, sym, wp, W, adj, rbase, rlen, rowid, nr, row_ctr, fl, lane);
+  else
+    stage_rows_t<false>(T, sym, wp, W, adj, rbase, rlen, rowid, nr, row_ctr, fl, lane);
 }
 
 // Heavy tier (d > 1024, the bitmap in global memory): the same row walk
