@@ -705,7 +705,7 @@ struct CtaArgs {
 // WS_GLOBAL -- everything in the global slice (sources too large for the
 // shared part).
 constexpr int WS_SMEM = 0, WS_SYM_GLOBAL = 1, WS_GLOBAL = 2;
-// WS_TILED: k = 4 totals of heavy sources (kcg_heavy.cuh) -- the bitmap in a
+// WS_TILED: k = 4 counts of heavy sources (kcg_heavy.cuh) -- the bitmap in a
 // global slice, counted through shared-memory tiles
 constexpr int WS_TILED = 3;
 
@@ -1172,23 +1172,30 @@ void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaS
   }
 }
 
-// Tiled heavy launch (k = 4 totals): 512-thread CTAs, two per SM when the
+// Tiled heavy launch (k = 4): 512-thread CTAs, two per SM when the
 // shared-memory plan allows it.
 constexpr int HV_NT = 512;
-inline unsigned heavy_grid(const HeavyArgs& hv, uint32_t nitems) {
-  auto kern = count_heavy4_kernel<HV_NT, 2>;
+template <bool PV>
+inline unsigned heavy_grid_t(const HeavyArgs& hv, uint32_t nitems) {
+  auto kern = count_heavy4_kernel<HV_NT, 2, PV>;
   KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(hv.smem_bytes)));
   int occ = 0;
   KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, HV_NT, hv.smem_bytes));
   return unsigned(std::min<uint64_t>(nitems, uint64_t(device().sms) * std::max(occ, 1)));
 }
+inline unsigned heavy_grid(const HeavyArgs& hv, uint32_t nitems) {
+  return hv.pv_rank ? heavy_grid_t<true>(hv, nitems) : heavy_grid_t<false>(hv, nitems);
+}
 void launch_heavy4(Graph& g, HeavyArgs hv, cudaStream_t st) {
   const unsigned grid = heavy_grid(hv, hv.nitems);
   if (size_t(grid) * hv.slice_words * 4 > g.heavy.n) fail(KCG_ERUNTIME, "heavy arena too small");
   hv.gbase = reinterpret_cast<uint32_t*>(g.heavy.p);
   KCG_CUDA(cudaMemsetAsync(hv.work, 0, 4, st));
-  count_heavy4_kernel<HV_NT, 2><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+  if (hv.pv_rank)
+    count_heavy4_kernel<HV_NT, 2, true><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+  else
+    count_heavy4_kernel<HV_NT, 2, false><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
   KCG_LAUNCHED(g);
   g.stats.launches++;
 }
@@ -1427,6 +1434,13 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       };
       std::vector<Plan> plans;
       const size_t smem_cap = size_t(dev.smem_optin) - 1024;
+      // the arena is sized before the launches: the plan already says which
+      // kernel (per-vertex or totals) it is for
+      auto tiled_plan = [&](uint32_t dmax) {
+        HeavyArgs hv = heavy_plan(dmax, HV_NT / 32, want_pv);
+        hv.pv_rank = want_pv ? PVR(g) : nullptr;
+        return hv;
+      };
       // a working set that does not fit shared memory: bitmap in global
       // memory and the rest in shared memory if that fits, else all global
       auto global_plan = [&](uint32_t lo, uint32_t hi, uint32_t dmax) {
@@ -1441,7 +1455,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       uint32_t pos = 0;
       while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
       if (pos) {
-        if (k == 4 && !want_pv && tiled_mode()) {
+        if (k == 4 && tiled_mode()) {
           // tiled kernel up to HV_DMAX in two bins (bucket table and tile
           // sizes follow the bin's largest source); beyond that the old path
           uint32_t p0 = 0;
@@ -1450,9 +1464,9 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
           uint32_t p1 = p0;
           while (p1 < pos && deg_at(p1) > 2047) p1++;
           if (p1 > p0)
-            plans.push_back({p0, p1, Layout{}, WS_TILED, HV_NT, heavy_plan(deg_at(p0), HV_NT / 32)});
+            plans.push_back({p0, p1, Layout{}, WS_TILED, HV_NT, tiled_plan(deg_at(p0))});
           if (pos > p1)
-            plans.push_back({p1, pos, Layout{}, WS_TILED, HV_NT, heavy_plan(deg_at(p1), HV_NT / 32)});
+            plans.push_back({p1, pos, Layout{}, WS_TILED, HV_NT, tiled_plan(deg_at(p1))});
         } else {
           global_plan(0, pos, deg_at(0));
         }

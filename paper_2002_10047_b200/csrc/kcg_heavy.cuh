@@ -49,11 +49,13 @@ struct HeavyArgs {
   uint32_t qs;         // tile row stride in quads (odd)
   uint32_t flag_stride;  // bytes per warp flag row
   uint32_t off_flags, off_tile_x, off_tile_i, off_queue;  // dynamic smem offsets
+  uint32_t off_pvl;    // per-vertex: u32 credits of the source's d local vertices
   uint32_t smem_bytes;
+  ull* pv_rank;        // per-vertex: global counts (rank space)
 };
 
 // dynamic shared memory plan for sources of out-degree <= dmax, NW warps
-inline HeavyArgs heavy_plan(uint32_t dmax, int nw) {
+inline HeavyArgs heavy_plan(uint32_t dmax, int nw, bool pv = false) {
   HeavyArgs a{};
   a.bbmax = bucket_bits(dmax);
   const uint32_t W = (dmax + 31) / 32, Q = (W + 3) / 4;
@@ -69,17 +71,19 @@ inline HeavyArgs heavy_plan(uint32_t dmax, int nw) {
   a.off_tile_i = uint32_t(tile);
   a.off_queue = uint32_t(2 * tile);
   const size_t phase_b = 2 * tile + size_t(nw) * 64 * 4;
-  a.smem_bytes = uint32_t(align_up(std::max(phase_a, phase_b), 128));
+  // per-vertex credits live through both phases (a source's credit per local
+  // vertex is at most C(d-1, 2) < 2^32)
+  a.off_pvl = uint32_t(align_up(std::max(phase_a, phase_b), 16));
+  a.smem_bytes = uint32_t(align_up(a.off_pvl + (pv ? size_t(dmax) * 4 : 0), 128));
   return a;
-}
-
-__device__ __forceinline__ uint32_t popc_and4(const uint4& a, const uint4& b) {
-  return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
 }
 
 // rows [row0, row0 + nrows) of the slice, quads [q0, q0 + qt) -> tile rows
 // of stride qs quads (all threads of the CTA; no barrier)
-template <int NT>
+// UPPER: the rows are symmetric and q0 is the quad of their own diagonal
+// block: bits at or below the row's index are cleared (they sit in the first
+// quad loaded).
+template <int NT, bool UPPER = false>
 __device__ __forceinline__ void heavy_load_tile(uint4* tile, const uint32_t* sym, uint32_t wp,
                                                 uint32_t row0, uint32_t nrows, uint32_t q0,
                                                 uint32_t qt, uint32_t qs) {
@@ -89,11 +93,21 @@ __device__ __forceinline__ void heavy_load_tile(uint4* tile, const uint32_t* sym
   if (sub >= rpp) return;
   for (uint32_t r = wib * rpp + sub; r < nrows; r += (NT / 32) * rpp) {
     const uint4* src = reinterpret_cast<const uint4*>(sym + size_t(row0 + r) * wp) + q0;
-    for (uint32_t c = q; c < qt; c += 32) tile[r * qs + c] = __ldcg(src + c);
+    for (uint32_t c = q; c < qt; c += 32) {
+      uint4 v = __ldcg(src + c);
+      if (UPPER && c == 0) {
+        const uint32_t wr = r >> 5, m = above_mask(r & 31);
+        v.x = wr > 0 ? 0u : wr == 0 ? v.x & m : v.x;
+        v.y = wr > 1 ? 0u : wr == 1 ? v.y & m : v.y;
+        v.z = wr > 2 ? 0u : wr == 2 ? v.z & m : v.z;
+        v.w = wr == 3 ? v.w & m : v.w;
+      }
+      tile[r * qs + c] = v;
+    }
   }
 }
 
-template <int NT, int MB>
+template <int NT, int MB, bool PV = false>
 __global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_src, s_row;
@@ -104,6 +118,7 @@ __global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
   uint4* tile_x = reinterpret_cast<uint4*>(smem + a.off_tile_x);
   uint4* tile_i = reinterpret_cast<uint4*>(smem + a.off_tile_i);
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem + a.off_queue) + wib * 64;
+  uint32_t* pvl = reinterpret_cast<uint32_t*>(smem + a.off_pvl);
   const uint32_t qs = a.qs;
   ull my_total = 0, my_staged = 0;
   auto grab = [&]() {
@@ -125,6 +140,9 @@ __global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
     const uint32_t W = (d + 31) / 32, Q = (W + 3) / 4, wp = 4 * Q;
     Buckets T = bucket_view(smem, bucket_bits(d), a.bbmax);
     bucket_clear(T, threadIdx.x, NT);
+    if constexpr (PV) {
+      for (uint32_t i = threadIdx.x; i < d; i += NT) pvl[i] = 0;
+    }
     for (uint32_t i = 4 * lane; i < a.flag_stride; i += 128)
       *reinterpret_cast<uint32_t*>(fl + i) = 0;  // the tiles of the last source lay here
     __syncthreads();
@@ -175,6 +193,92 @@ __global__ void __launch_bounds__(NT, MB) count_heavy4_kernel(HeavyArgs a) {
         stage_scan<false>(T, fl, lane, next, emit);
     }
     __syncthreads();  // the slice's rows are visible to the whole CTA
+    if constexpr (PV) {
+      // ---- per-vertex: symmetric rows.  Edge (i, x), i < x, credits x with
+      // all = |N+(i) ∩ N(x)| over the columns above i -- x as the middle
+      // vertex of (i, x, y), y > x, and as the top vertex of (i, y, x),
+      // i < y < x -- and i with cx, the part above x (clique_rec.hpp:33-36,
+      // counting.cpp:191-198).  Row block I stays resident, masked to the bits
+      // above each row's index; the symmetric row blocks X >= I stream
+      // through the second tile, both from I's own quad on.
+      mirror_lower(sym, wp, d, W, wib, NT / 32, lane);
+      __syncthreads();
+      ull acc = 0;
+      uint32_t qn = 0;
+      for (uint32_t bi = 0; bi < Q; bi++) {
+        const uint32_t qt = Q - bi;
+        const uint32_t ni = min(HV_TB, d - HV_TB * bi);
+        heavy_load_tile<NT, true>(tile_i, sym, wp, HV_TB * bi, ni, bi, qt, qs);
+        for (uint32_t bx = bi; bx < Q; bx++) {
+          const uint32_t nx = min(HV_TB, d - HV_TB * bx);
+          const uint32_t qx = bx - bi;
+          heavy_load_tile<NT>(tile_x, sym, wp, HV_TB * bx, nx, bi, qt, qs);
+          if (threadIdx.x == 0) s_row = 0;
+          __syncthreads();
+          auto run_batch = [&](bool valid) {
+            const uint32_t e = valid ? queue[lane] : 0u;
+            const uint32_t r = e >> 8, xl = e & 255u;
+            const uint4* pi = tile_i + r * qs;
+            const uint4* px = tile_x + xl * qs;
+            uint32_t lo = 0, hi = 0;
+            for (uint32_t q = 0; q < qx; q++) lo += popc_and4(pi[q], px[q]);
+            for (uint32_t q = qx + 1; q < qt; q++) hi += popc_and4(pi[q], px[q]);
+            // x's own quad: everything counts for `all`, bits above x for cx
+            const uint4 va = pi[qx], vb = px[qx];
+            const uint32_t m[4] = {va.x & vb.x, va.y & vb.y, va.z & vb.z, va.w & vb.w};
+            const uint32_t wx = xl >> 5, mx = above_mask(xl & 31);
+            uint32_t mid = 0, midx = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 4; j++) {
+              mid += __popc(m[j]);
+              midx += __popc(j < wx ? 0u : j == wx ? m[j] & mx : m[j]);
+            }
+            if (valid) {
+              const uint32_t all = lo + mid + hi, cx = midx + hi;
+              if (all) atomicAdd(&pvl[HV_TB * bx + xl], all);
+              if (cx) atomicAdd(&pvl[HV_TB * bi + r], cx);
+              acc += cx;
+            }
+          };
+          for (;;) {
+            const uint32_t r = grab();
+            if (r >= ni) break;
+            const uint4 m4 = tile_i[r * qs + qx];
+            const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              const uint32_t v = mw[j];
+              if (v == 0) continue;
+              if ((v >> lane) & 1u) queue[qn + __popc(v & lt)] = (r << 8) | (32u * j + lane);
+              qn += __popc(v);
+              if (qn >= 32) {
+                __syncwarp();
+                const bool mv = lane + 32 < qn;
+                const uint32_t e1 = mv ? queue[lane + 32] : 0u;
+                run_batch(true);
+                __syncwarp();
+                if (mv) queue[lane] = e1;
+                qn -= 32;
+                __syncwarp();
+              }
+            }
+          }
+          __syncwarp();
+          if (qn) run_batch(lane < qn);
+          qn = 0;
+          __syncthreads();
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0 && acc) {
+        my_total += acc;
+        atomicAdd(&a.pv_rank[u], acc);
+      }
+      // (the last pair's closing barrier ordered every credit before this)
+      for (uint32_t i = threadIdx.x; i < d; i += NT)
+        if (pvl[i]) atomicAdd(&a.pv_rank[__ldg(a.adj + b + i)], ull(pvl[i]));
+      continue;
+    }
     // ---- tiled triangle count of the induced DAG
     ull acc = 0;
     uint32_t qn = 0;  // (i, x) queue length, warp-uniform

@@ -23,6 +23,10 @@ namespace kcg {
 namespace {
 
 constexpr ull EMPTY64 = ~0ull;
+
+__device__ __forceinline__ uint32_t popc_and4(const uint4& a, const uint4& b) {
+  return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+}
 constexpr int STAGE_U = 4;
 
 // Open-addressing table of (key | local index << 32) plus a filter.
@@ -444,12 +448,13 @@ template <bool OVF, class Next, class Emit>
 __device__ __forceinline__ void stage_scan(const Buckets& T, uint8_t* fl, uint32_t lane, Next next,
                                            Emit emit) {
   const uint32_t NF = (1u << T.bb) - 1;
+  // any non-zero byte marks a hit: NF's low byte is 0x7f or 0xff
   auto probe = [&](uint32_t y) {
     const uint32_t j = bucket_probe<OVF>(T, y);
-    if (j < NF) fl[j] = 1;
+    if (j < NF) fl[j] = uint8_t(NF);
   };
   StageRow cur{0, 0, nullptr}, nxt{0, 0, nullptr};
-  uint32_t y[STAGE_U];
+  uint32_t y[STAGE_U], yn[STAGE_U];
   if (!next(cur)) return;
   stage_load(cur.src, cur.len, lane, y);
   for (;;) {
@@ -457,20 +462,24 @@ __device__ __forceinline__ void stage_scan(const Buckets& T, uint8_t* fl, uint32
     if (!have_next) nxt.len = 0;
     const uint32_t* s = cur.src;
     uint32_t rem = cur.len;
-    for (;;) {
-      const bool more = rem > 128;
-      uint32_t yn[STAGE_U];
-      stage_load(more ? s + 128 : nxt.src, more ? rem - 128 : nxt.len, lane, yn);
-      probe(y[0]);
-      if (rem > 32) probe(y[1]);
-      if (rem > 64) probe(y[2]);
-      if (rem > 96) probe(y[3]);
-#pragma unroll
-      for (int v = 0; v < STAGE_U; v++) y[v] = yn[v];
-      if (!more) break;
+    // full chunks with more of the row behind them
+    while (rem > 128) {
       s += 128;
       rem -= 128;
+      stage_load(s, rem, lane, yn);
+#pragma unroll
+      for (int v = 0; v < STAGE_U; v++) probe(y[v]);
+#pragma unroll
+      for (int v = 0; v < STAGE_U; v++) y[v] = yn[v];
     }
+    // the row's last chunk, the next row's first chunk behind it
+    stage_load(nxt.src, nxt.len, lane, yn);
+    probe(y[0]);
+    if (rem > 32) probe(y[1]);
+    if (rem > 64) probe(y[2]);
+    if (rem > 96) probe(y[3]);
+#pragma unroll
+    for (int v = 0; v < STAGE_U; v++) y[v] = yn[v];
     __syncwarp();
     emit(cur);
     __syncwarp();
@@ -510,7 +519,7 @@ __device__ __forceinline__ void stage_rows_t(const Buckets& T, uint32_t* sym, ui
       const uint32_t b1 = __ballot_sync(FULL, x & 0x0000ff00u);
       const uint32_t b2 = __ballot_sync(FULL, x & 0x00ff0000u);
       const uint32_t b3 = __ballot_sync(FULL, x & 0xff000000u);
-      if (lane < 4) dst[4 * g + lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
+      if (lane == 0) *reinterpret_cast<uint4*>(dst + 4 * g) = make_uint4(b0, b1, b2, b3);
     }
   };
   stage_scan<OVF>(T, fl, lane, next, emit);

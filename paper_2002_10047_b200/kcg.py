@@ -97,7 +97,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return os.path.join(LIB_DIR, "libkcg.so")
+    # KCG_LIB: a variant build of the same library (tools/ab_build.sh A/B runs)
+    return os.environ.get("KCG_LIB") or os.path.join(LIB_DIR, "libkcg.so")
 
 
 def lib():
