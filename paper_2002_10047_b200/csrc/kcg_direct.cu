@@ -28,6 +28,10 @@ constexpr int kThreads = 256;
 // walking a 50k-entry slice with dependent gathers was the long tail of
 // both passes on the skewed configs.
 constexpr uint32_t kHubDeg = 2048;
+// Hub CTAs are latency-bound on the rank gathers: four 512-thread CTAs per SM
+// (one per SM left three quarters of the warp slots empty: config 5 hub passes
+// 2.9 + 4.6 ms).
+constexpr unsigned kHubGrid = 148 * 4;
 
 __global__ void outdeg_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                               const uint32_t* __restrict__ rank, uint32_t n,
@@ -42,12 +46,18 @@ __global__ void outdeg_kernel(const uint64_t* __restrict__ off, const uint32_t* 
       if (lane == 0) hubs[atomicAdd(nhubs, 1u)] = uint32_t(u);
       continue;
     }
+    // four 32-entry chunks per step: the adjacency loads, then the rank
+    // gathers, are all in flight together (a 2048-entry slice was 64
+    // dependent load pairs in a row)
     uint32_t c = 0;
-    for (uint64_t p0 = b; p0 < e; p0 += 32) {
-      uint64_t p = p0 + lane;
-      bool out = p < e && rank[adj[p]] > ru;
-      c += __popc(__ballot_sync(0xffffffffu, out));
+    for (uint64_t p0 = b + lane; p0 < e; p0 += 128) {
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = p0 + 32 * j < e ? adj[p0 + 32 * j] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < 4; j++) c += v[j] != 0xffffffffu && rank[v[j]] > ru;
     }
+    c = __reduce_add_sync(0xffffffffu, c);
     if (lane == 0) {
       if (outdeg) outdeg[u] = c;
       rdeg[ru] = c;
@@ -123,25 +133,27 @@ __global__ void __launch_bounds__(256)
     const uint32_t dout = uint32_t(rdag_off[ru + 1] - wr0);
     const bool shortl = dout <= 32;
     uint32_t got = 0;
-    for (uint64_t p0 = b; p0 < e && got < dout; p0 += 32) {
-      const uint64_t p = p0 + lane;
-      uint32_t v = 0, rv = 0;
-      bool out = false;
-      if (p < e) {
-        v = adj[p];
-        rv = rank[v];
-        out = rv > ru;
+    // four chunks per step, loads and gathers in flight together
+    for (uint64_t p0 = b + lane; p0 < e + lane && got < dout; p0 += 128) {
+      uint32_t v[4], rv[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) v[j] = p0 + 32 * j < e ? adj[p0 + 32 * j] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < 4; j++) rv[j] = v[j] != 0xffffffffu ? rank[v[j]] : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const bool out = rv[j] > ru;  // ranks of real targets only: padding has rank 0 <= ru
+        const unsigned ball = __ballot_sync(0xffffffffu, out);
+        if (out) {
+          const uint32_t at = got + __popc(ball & ((1u << lane) - 1));
+          if (dag_adj) dag_adj[wid + at] = v[j];
+          if (shortl)
+            buf[wib][at] = rv[j];
+          else
+            rdag_adj[wr0 + at] = rv[j];
+        }
+        got += __popc(ball);
       }
-      const unsigned ball = __ballot_sync(0xffffffffu, out);
-      if (out) {
-        const uint32_t at = got + __popc(ball & ((1u << lane) - 1));
-        if (dag_adj) dag_adj[wid + at] = v;
-        if (shortl)
-          buf[wib][at] = rv;
-        else
-          rdag_adj[wr0 + at] = rv;
-      }
-      got += __popc(ball);
     }
     if (shortl) {
       if (dout) {
@@ -394,7 +406,7 @@ void build_dag(Graph& g, bool want_id_dag) {
     outdeg_kernel<<<grid, kThreads, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n, odeg,
                                                    rdeg, hubs, cnt + 2);
     KCG_LAUNCHED(g);
-    outdeg_hub_kernel<<<148, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, hubs,
+    outdeg_hub_kernel<<<kHubGrid, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, hubs,
                                                  cnt + 2, odeg, rdeg);
     KCG_LAUNCHED(g);
   }
@@ -406,7 +418,7 @@ void build_dag(Graph& g, bool want_id_dag) {
                                                  want_id_dag ? g.dag_adj.p : nullptr,
                                                  g.rdag_off.p, g.rdag_adj.p, lists, cnt);
     KCG_LAUNCHED(g);
-    fill_hub_kernel<<<148, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n, hubs,
+    fill_hub_kernel<<<kHubGrid, 512, 0, g.stream>>>(g.und_off.p, g.und_adj.p, g.rank.p, n, hubs,
                                                cnt + 2, want_id_dag ? g.dag_off.p : nullptr,
                                                want_id_dag ? g.dag_adj.p : nullptr, g.rdag_off.p,
                                                g.rdag_adj.p, lists, cnt);
