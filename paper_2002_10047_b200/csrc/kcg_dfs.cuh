@@ -18,10 +18,10 @@
 // unchosen candidates (N stays shared), so no lane waits on another's
 // subtree.
 //
-// Per-vertex counts (PV): a leaf node (two vertices still to choose)
-// credits every v ∈ N with its degree inside N when it is created; every
-// other chosen vertex is credited with its subtree count when its node is
-// popped; a lane finishing a stolen node credits the whole chain above it.
+// Per-vertex counts (PV): inside a leaf node (two vertices still to choose)
+// every v ∈ N is credited with its degree inside N; every other chosen
+// vertex is credited with its subtree count when its node is done; a lane
+// finishing a stolen node credits the whole chain above it.
 #pragma once
 
 namespace kcg {
@@ -110,12 +110,33 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
     if constexpr (PV) st.X[0][lane] = root_v;
   }
   if constexpr (PV) leaf_pv_collect(lvl == 0 && R == 2, N0, my_sym, lane, acc);
+  // A node with three vertices still to choose is never pushed: choosing x
+  // there leaves the leaf node lN = N ∩ N+(x), whose pairs are counted by an
+  // inner loop over y ∈ lN held in registers (lJ = the y not yet visited).
+  // These are most of the tree's nodes, so the stack only sees the levels
+  // above them.  PV: y is credited with its degree inside lN (every pair
+  // (y, z) of lN closes one clique and credits both ends), x with the
+  // node's count when the loop ends.
+  uint32_t lN = 0, lJ = 0, lx = 0;
+  pvc_t lsum = 0;
   for (;;) {
 #pragma unroll
     for (int t = 0; t < DFS_STEPS; t++) {
-      bool made_leaf = false;
-      uint32_t leafN = 0;
-      if (lvl >= base) {
+      if (lJ) {
+        const int y = __ffs(lJ) - 1;
+        lJ &= lJ - 1;
+        const uint32_t cs = __popc(lN & usym[y]);
+        total += cs;
+        if constexpr (PV) {
+          lsum += cs;
+          const uint32_t ca = __popc(lN & sym[y]);
+          if (ca) atomicAdd(&cpv[y], pvc_t(ca));
+          if (lJ == 0) {
+            if (lsum) atomicAdd(&cpv[lx], lsum);
+            csub += lsum;
+          }
+        }
+      } else if (lvl >= base) {
         if (cI == 0) {
           // node exhausted: credit and pop
           if constexpr (PV) {
@@ -142,6 +163,14 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
           if (r == 2) {
             total += cs;
             if constexpr (PV) csub += cs;
+          } else if (r == 3) {
+            if (cs >= 2) {
+              lN = lJ = child;
+              if constexpr (PV) {
+                lx = x;
+                lsum = 0;
+              }
+            }
           } else if (cs >= uint32_t(r - 1)) {
             st.ni[lvl][lane] = make_uint2(cN, cI);
             if (cI & (cI - 1)) smask |= 1u << lvl;
@@ -149,15 +178,12 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
               st.sub[lvl][lane] = csub;
               csub = 0;
               st.X[lvl + 1][lane] = x;
-              made_leaf = r - 1 == 2;
-              leafN = child;
             }
             lvl++;
             cN = cI = child;
           }
         }
       }
-      if constexpr (PV) leaf_pv_collect(made_leaf, leafN, my_sym, lane, acc);
     }
     const bool busy = lvl >= base;
     const unsigned busym = __ballot_sync(FULLM, busy);
