@@ -46,6 +46,8 @@ constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t NOTFOUND = 0xffffffffu;
 constexpr int WARP_THREADS_BLOCK = 256;
 constexpr int WARP_TIER_WARPS = WARP_THREADS_BLOCK / 32;
+constexpr uint32_t WARP_TABLE_BITS = 7;  // 128 buckets for <= 32 keys
+constexpr size_t WARP_TABLE_BYTES = 128 * 20 + 128 / 8 + 64 * 8 + 16;  // bucket_bytes(32)
 constexpr uint32_t SMEM_TIER_MAX = 1024;  // largest d staged in shared memory
 
 __device__ __forceinline__ uint32_t above_mask(uint32_t b) {  // bits > b, b in [0,31]
@@ -80,17 +82,13 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     count_warp_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                       const uint32_t* __restrict__ srcs, uint32_t nsrc, int k,
                       ull* __restrict__ total_out, ull* __restrict__ pv_rank,
-                      ull* __restrict__ staged_out, int combine) {
+                      ull* __restrict__ staged_out) {
   struct WarpSmem {
-    ull table[64];
-    ull rbase[32];
+    alignas(16) unsigned char tbl[WARP_TABLE_BYTES];  // Buckets for <= 32 keys (B = 128)
+    alignas(16) uint32_t fl[32];                      // staging flag row (one bitmap word)
     uint32_t sym[32];
     uint32_t usym[32];
-    uint32_t P[34];
-    uint32_t rowid[32];
-    uint32_t filter[16];
     uint32_t map[32];
-    uint32_t qy[64], qi[64];
   };
   __shared__ WarpSmem s_w[WARP_TIER_WARPS];
   __shared__ pvc_t s_pv[PV ? WARP_TIER_WARPS : 1][32];
@@ -101,9 +99,9 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
   Stacks<PV, SL>* stk = reinterpret_cast<Stacks<PV, SL>*>(dyn_smem) + wib;
   uint32_t* sym = S.sym;
   pvc_t* cpv = s_pv[PV ? wib : 0];
-  const Member M{S.table, S.filter, 6, 9};
   const int R = k - 2;
   ull my_total = 0, my_staged = 0;
+  S.fl[lane] = 0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t si = gw; si < nsrc; si += nw) {
@@ -111,9 +109,6 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
     const uint64_t b = off[u];
     const uint32_t d = uint32_t(off[u + 1] - b);
     const uint32_t w = lane < d ? adj[b + lane] : 0u;
-    S.table[lane] = EMPTY64;
-    S.table[lane + 32] = EMPTY64;
-    if (lane < 16) S.filter[lane] = 0;
     sym[lane] = 0;
     if constexpr (PV) cpv[lane] = 0;
     uint64_t sb = 0;
@@ -122,47 +117,26 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
       sb = off[w];
       len = uint32_t(off[w + 1] - sb);
     }
+    // N+(u) in the warp's bucketed membership table (kcg_stage.cuh), index
+    // field = flag position of the local index
+    Buckets T = bucket_view(S.tbl, WARP_TABLE_BITS, WARP_TABLE_BITS);
+    for (uint32_t attempt = 0;; attempt++) {
+      T.mul = BKT_HASH + 2u * 0x632BE5ABu * attempt;
+      T.ovf_mode = attempt >= BKT_TRIES;
+      __syncwarp();
+      bucket_clear(T, lane, 32);
+      __syncwarp();
+      const bool ok = lane < d ? bucket_insert(T, w, flag_pos(lane)) : true;
+      if (__all_sync(FULL, ok)) break;
+    }
     __syncwarp();
-    if (lane < d) member_insert(M, w, lane);
     // Row i either is scanned (len entries) or searched: its d-1-i
     // candidate targets w_j (j > i) are binary-searched in N+(w_i), which
     // costs (d-1-i) * log2(len) probes -- cheaper for the long rows that
     // small sources point into.
     const uint32_t tg = lane < d ? d - 1 - lane : 0u;
     const bool srch = tg > 0 && tg * (32u - __clz(len)) < len;
-    // split the other non-empty rows into long (>= 32) and short ones,
-    // each list compacted with its own prefix of lengths; long rows at
-    // [0, nl), short rows at [nl, nl + ns) with their prefix at P[nl + 1 ..]
-    const bool lg = !srch && len >= 32, sh = !srch && len > 0 && len < 32;
-    const unsigned ml = __ballot_sync(FULL, lg), ms = __ballot_sync(FULL, sh);
-    const uint32_t nl = __popc(ml), ns = __popc(ms);
-    uint32_t il = lg ? len : 0, is = sh ? len : 0;
-    for (int s = 1; s < 32; s <<= 1) {
-      const uint32_t tl = __shfl_up_sync(FULL, il, s), ts = __shfl_up_sync(FULL, is, s);
-      if (lane >= uint32_t(s)) {
-        il += tl;
-        is += ts;
-      }
-    }
-    const uint32_t Ll = __shfl_sync(FULL, il, 31), Ls = __shfl_sync(FULL, is, 31);
-    const unsigned below = (1u << lane) - 1;
-    if (lg) {
-      const uint32_t ci = __popc(ml & below);
-      S.P[ci] = il - len;
-      S.rbase[ci] = sb;
-      S.rowid[ci] = lane;
-    } else if (sh) {
-      const uint32_t ci = __popc(ms & below);
-      S.P[nl + 1 + ci] = is - len;
-      S.rbase[nl + ci] = sb;
-      S.rowid[nl + ci] = lane;
-    }
-    if (lane == 0) {
-      S.P[nl] = Ll;
-      S.P[nl + 1 + ns] = Ls;
-    }
     my_staged += srch ? 0u : len;
-    __syncwarp();
     {
       // searched rows: tasks (i, j) flattened over the lanes
       uint32_t ti = srch ? tg : 0u;
@@ -170,9 +144,9 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
         const uint32_t t = __shfl_up_sync(FULL, ti, s);
         if (lane >= uint32_t(s)) ti += t;
       }
-      const uint32_t T = __shfl_sync(FULL, ti, 31);
+      const uint32_t T_ = __shfl_sync(FULL, ti, 31);
       const uint32_t tex = ti - (srch ? tg : 0u);
-      for (uint32_t t0 = 0; t0 < T; t0 += 32) {
+      for (uint32_t t0 = 0; t0 < T_; t0 += 32) {
         const uint32_t t = t0 + lane;
         uint32_t r = 0;
 #pragma unroll
@@ -186,7 +160,7 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
         const uint32_t rl = __shfl_sync(FULL, len, r);
         const uint32_t j = r + 1 + (t - rt);
         const uint32_t target = __shfl_sync(FULL, w, j & 31);
-        if (t < T) {
+        if (t < T_) {
           // lower_bound(target) in the sorted row adj[rb, rb + rl)
           uint32_t lo = 0, n = rl;
           while (n > 1) {
@@ -200,13 +174,37 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
           }
         }
       }
-      my_staged += T;
-      Stager<PV> st{M, sym, 1, S.qy, S.qi, lane, 0, combine != 0};
-      const Rows rl{S.P, S.rbase, S.rowid, nl};
-      stage_long(rl, st, adj, 0, Ll);
-      const Rows rs{S.P + nl + 1, S.rbase + nl, S.rowid + nl, ns};
-      stage_short(rs, st, adj, 0, Ls);
-      st.flush();
+      my_staged += T_;
+      // scanned rows, one after the other through the row scan of the CTA
+      // tiers (kcg_stage.cuh: stage_scan); a row is one bitmap word, which
+      // lane i keeps in a register (PV: plus the mirrored bits)
+      uint32_t scanm = __ballot_sync(FULL, !srch && len > 0);
+      uint32_t symr = 0;
+      auto next = [&](StageRow& row) {
+        if (scanm == 0) return false;
+        const int r = __ffs(scanm) - 1;
+        scanm &= scanm - 1;
+        row.i = uint32_t(r);
+        row.len = __shfl_sync(FULL, len, r);
+        row.src = adj + __shfl_sync(FULL, sb, r);
+        return true;
+      };
+      auto emit = [&](const StageRow& row) {
+        const uint32_t x = S.fl[lane];
+        if (x) S.fl[lane] = 0;
+        const uint32_t word = __ballot_sync(FULL, x != 0);
+        if (lane == row.i) symr |= word;
+        if constexpr (PV) {
+          if ((word >> lane) & 1u) symr |= 1u << row.i;
+        }
+      };
+      uint8_t* fl8 = reinterpret_cast<uint8_t*>(S.fl);
+      if (T.ovf_mode)
+        stage_scan<true>(T, fl8, lane, next, emit);
+      else
+        stage_scan<false>(T, fl8, lane, next, emit);
+      __syncwarp();
+      sym[lane] |= symr;
     }
     __syncwarp();
     S.usym[lane] = sym[lane] & above_mask(lane);
@@ -690,7 +688,6 @@ struct CtaArgs {
   unsigned* work;        // work-item counter
   unsigned char* gbase;  // global working sets (heavy tier)
   Layout L;
-  int combine;           // Stager: pre-combine same-word hits
 };
 
 // GWS = false: the whole working set is dynamic shared memory (the
@@ -1219,18 +1216,6 @@ inline uint32_t slices_for(uint32_t d, int k) {
   return std::min<uint32_t>(64, d / 64);
 }
 
-// Pre-combining of same-word staging hits (Stager::set): 2 = warp tier only
-// (default: its rows are single words, so a batch's hits collide; config 4
-// k=6 50.4 -> 46.4 ms, per-vertex 211.6 -> 182.3 ms), 1 = every tier
-// (config 2 k=4 12.97 -> 13.94 ms), 0 = off.  KCG_COMBINE overrides.
-inline int combine_mode() {
-  static const int m = [] {
-    const char* e = getenv("KCG_COMBINE");
-    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
-  }();
-  return m;
-}
-
 // KCG_TILED=0 sends heavy k = 4 sources down the older global-bitmap path
 inline bool tiled_mode() {
   static const bool m = [] {
@@ -1371,8 +1356,7 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       auto run = [&](auto kern) {
         KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
         kern<<<grid, WARP_THREADS_BLOCK, dsm, aux_stream(false)>>>(g.rdag_off.p, g.rdag_adj.p, wlist, nw, k,
-                                                          ctr, PVR(g), ctr + 1,
-                                                          combine_mode() != 0);
+                                                          ctr, PVR(g), ctr + 1);
       };
       if (want_pv)
         k <= 4 ? run(count_warp_kernel<true, 0>)
@@ -1418,7 +1402,6 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       a.total = ctr;
       a.pv_rank = PVR(g);
       a.staged = ctr + 1;
-      a.combine = combine_mode() == 1;
       const size_t budget = size_t(8) << 30;
       const uint32_t levels = std::max<uint32_t>(R, 1);
       const bool big = k > 10;  // DFS engine stack depth 32 instead of 8
