@@ -1216,6 +1216,21 @@ inline uint32_t slices_for(uint32_t d, int k) {
   return std::min<uint32_t>(64, d / 64);
 }
 
+// Smallest out-degree (exclusive) the tiled k = 4 kernel takes; a bin bound
+// of the shared-memory tier.  Default 512: above that the shared-memory tier
+// holds one or two CTAs per SM (bitmaps of 70-130 KB), while tiles of the
+// L2-resident slice leave room for two 512-thread CTAs with any d (config 5
+// k=4 count 1317 -> 1237 ms, per-vertex 2171 -> 1845 ms; config 2 9.20 ->
+// 8.97 ms).  KCG_TILED_FROM overrides (256, 362, 512, 724, 1024).
+inline uint32_t tiled_from() {
+  static const uint32_t m = [] {
+    const char* e = getenv("KCG_TILED_FROM");
+    const long v = e ? atol(e) : 0;
+    return uint32_t(v == 256 || v == 362 || v == 512 || v == 724 || v == 1024 ? v : 512);
+  }();
+  return m;
+}
+
 // KCG_TILED=0 sends heavy k = 4 sources down the older global-bitmap path
 inline bool tiled_mode() {
   static const bool m = [] {
@@ -1434,22 +1449,27 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
           plans.push_back({lo, hi, make_layout(dmax, levels, want_pv, 16, sbytes), WS_GLOBAL,
                            512, HeavyArgs{}});
       };
-      // heavy: d > SMEM_TIER_MAX
+      // heavy: d > smem_max (k = 4: the tiled kernel may start lower than
+      // the largest bitmap shared memory can hold, see tiled_from)
+      const bool tiled = k == 4 && tiled_mode();
+      const uint32_t smem_max = tiled ? tiled_from() : SMEM_TIER_MAX;
       uint32_t pos = 0;
-      while (pos < nc && deg_at(pos) > SMEM_TIER_MAX) pos++;
+      while (pos < nc && deg_at(pos) > smem_max) pos++;
       if (pos) {
-        if (k == 4 && tiled_mode()) {
-          // tiled kernel up to HV_DMAX in two bins (bucket table and tile
-          // sizes follow the bin's largest source); beyond that the old path
+        if (tiled) {
+          // tiled kernel up to HV_DMAX, binned (bucket table and tile sizes
+          // follow the bin's largest source); beyond that the old path
           uint32_t p0 = 0;
           while (p0 < pos && deg_at(p0) > HV_DMAX) p0++;
           if (p0) global_plan(0, p0, deg_at(0));
-          uint32_t p1 = p0;
-          while (p1 < pos && deg_at(p1) > 2047) p1++;
-          if (p1 > p0)
-            plans.push_back({p0, p1, Layout{}, WS_TILED, HV_NT, tiled_plan(deg_at(p0))});
-          if (pos > p1)
-            plans.push_back({p1, pos, Layout{}, WS_TILED, HV_NT, tiled_plan(deg_at(p1))});
+          const uint32_t tb[] = {2047, 1024, 724, 512, 362, 256, 0};
+          for (uint32_t lo : tb) {
+            uint32_t p1 = p0;
+            while (p1 < pos && deg_at(p1) > lo) p1++;
+            if (p1 > p0)
+              plans.push_back({p0, p1, Layout{}, WS_TILED, HV_NT, tiled_plan(deg_at(p0))});
+            p0 = p1;
+          }
         } else {
           global_plan(0, pos, deg_at(0));
         }
