@@ -130,6 +130,10 @@ __global__ void __launch_bounds__(WARP_THREADS_BLOCK)
       if (__all_sync(FULL, ok)) break;
     }
     __syncwarp();
+#if KCG_FILTER
+    bucket_filter(T, lane, 32);
+    __syncwarp();
+#endif
     // Row i either is scanned (len entries) or searched: its d-1-i
     // candidate targets w_j (j > i) are binary-searched in N+(w_i), which
     // costs (d-1-i) * log2(len) probes -- cheaper for the long rows that

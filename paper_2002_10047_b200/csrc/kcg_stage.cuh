@@ -6,6 +6,9 @@
 // (proj/src/counting.cpp:21-48); here N+(u) sits in a shared-memory bucketed
 // table and warps scan whole rows N+(w_i) against it.
 #pragma once
+#ifndef KCG_FILTER
+#define KCG_FILTER 1
+#endif
 
 namespace kcg {
 namespace {
@@ -155,11 +158,25 @@ __device__ __forceinline__ uint32_t bucket_probe(const Buckets& T, uint32_t y) {
   const uint32_t h = y * T.mul;
   const uint32_t b = h >> (32 - T.bb);
   const uint32_t t = h << T.bb;
-  const uint4 q = T.keys[b];
-  uint32_t j = min(min(q.x - t, q.y - t), min(q.z - t, q.w - t));
+  uint32_t j = 0xffffffffu;
+#if KCG_FILTER
+  // one filter word per bucket (bucket_filter): bit = the top five tag bits.
+  // A scattered LDS.32 costs ~3.4 wavefronts per warp against ~8.7 for the
+  // scattered LDS.128 of the buckets, which only the few filter-positive
+  // lanes now issue -- the staging loops run at 86-99 % of the LSU
+  // wavefront peak (profiles/r02_notes.md).
+  const bool maybe = (T.cnt[b] >> (t >> 27)) & 1u;
+#else
+  const bool maybe = true;
+#endif
+  uint4 q = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+  if (maybe) {
+    q = T.keys[b];
+    j = min(min(q.x - t, q.y - t), min(q.z - t, q.w - t));
+  }
   if constexpr (OVF) {
     const uint32_t B = 1u << T.bb;
-    const bool full_miss = j >= B - 1 && y != EMPTY && q.w != EMPTY;
+    const bool full_miss = maybe && j >= B - 1 && y != EMPTY && q.w != EMPTY;
     if (__any_sync(FULL, full_miss)) {
       if (full_miss && ((T.flag[b >> 5] >> (b & 31)) & 1u)) {
         const uint32_t no = min(*T.ovf_n, BKT_OVF_CAP);
@@ -171,6 +188,24 @@ __device__ __forceinline__ uint32_t bucket_probe(const Buckets& T, uint32_t y) {
     }
   }
   return j;
+}
+
+// After the inserts (and a barrier): the insert counts become the buckets'
+// filter words, one bit per key at the top five bits of its slot (the tag
+// bits right below the bucket index); overflowed buckets pass everything.
+// The caller synchronises afterwards.
+__device__ __forceinline__ void bucket_filter(const Buckets& T, uint32_t t, uint32_t nt) {
+  const uint32_t B = 1u << T.bb;
+  for (uint32_t b = t; b < B; b += nt) {
+    const uint4 q = T.keys[b];
+    uint32_t w = 0;
+    if (q.x != EMPTY) w |= 1u << (q.x >> 27);
+    if (q.y != EMPTY) w |= 1u << (q.y >> 27);
+    if (q.z != EMPTY) w |= 1u << (q.z >> 27);
+    if (q.w != EMPTY) w |= 1u << (q.w >> 27);
+    if (T.ovf_mode && ((T.flag[b >> 5] >> (b & 31)) & 1u)) w = 0xffffffffu;
+    T.cnt[b] = w;
+  }
 }
 
 // Builds the table for the d keys adj[0..d) (all threads of the CTA; ends
@@ -189,8 +224,12 @@ __device__ __forceinline__ void bucket_build(Buckets& T, const uint32_t* __restr
     bool ok = true;
     for (uint32_t i = t; i < d; i += nt)
       ok &= bucket_insert(T, keys[i], FLAGPOS ? flag_pos(i) : i);
-    if (__syncthreads_and(ok)) return;
+    if (__syncthreads_and(ok)) break;
   }
+#if KCG_FILTER
+  bucket_filter(T, t, nt);
+  __syncthreads();
+#endif
 }
 
 // 128 entries (or the `rem` < 128 left, EMPTY beyond) at s -> z
