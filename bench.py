@@ -209,15 +209,62 @@ def roofline_entry(cid, k, n, m, sum_io, count_ms, peaks, ops, l2_bytes, per_ver
     return e
 
 
-def ncu_entry(cfg_id, k):
-    """The committed ncu capture of one counting call (profiles/)."""
+def phase_rooflines(strat, n, m, rank_ms, direct_ms, peaks):
+    """SURVEY.md §8(d) byte formulas for the streaming phases against measured
+    HBM: degree ranking 8(n+1) + 4n; DAG build 16(n+1) + 8m + 8m + 4n + 4m
+    (offsets, adjacency, rank gathers, writes).  The round-based rankings read
+    at least 5n + 8(n+1) + 8m (first round's scan + every adjacency entry once):
+    quoted as a lower bound on their bytes."""
+    hbm = peaks["hbm_gbs"]
+    out = {}
+    if strat == 0:
+        rb, note = 8.0 * (n + 1) + 4.0 * n, "degree: 8(n+1) + 4n"
+    else:
+        rb, note = 5.0 * n + 8.0 * (n + 1) + 8.0 * m, "lower bound: 5n + 8(n+1) + 8m"
+    if rank_ms:
+        out["rank"] = {"alg_bytes": rb, "formula": note, "ms": rank_ms, "bound": "hbm",
+                       "achieved": rb / (rank_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                       "frac": rb / (rank_ms / 1e3) / 1e9 / hbm}
+    db = 16.0 * (n + 1) + 20.0 * m + 4.0 * n
+    if direct_ms:
+        out["direct"] = {"alg_bytes": db, "formula": "16(n+1) + 8m + 8m + 4n + 4m", "ms": direct_ms,
+                         "bound": "hbm", "achieved": db / (direct_ms / 1e3) / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": db / (direct_ms / 1e3) / 1e9 / hbm}
+    return out
+
+
+def ncu_entry(cfg_id, k, pv=False):
+    """The committed ncu counters of one counting call (profiles/ncu_summary.json,
+    written by tools/ncu_counts.py on the B200)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
         return None
     try:
-        return json.load(open(path)).get(f"config{cfg_id}_k{k}")
+        return json.load(open(path)).get(f"config{cfg_id}_k{k}" + ("_pv" if pv else ""))
     except ValueError:
         return None
+
+
+def attach_ncu(roofline, ncu):
+    """ncu's own view of what binds the counting kernels, next to the algorithmic
+    roof: DRAM and L2 bytes of one count, and the two busiest units, time-weighted
+    over the count's launches -- the LSU data pipe (shared-memory and global
+    wavefronts: the staging probes and the bitmap rows) and the issue slots."""
+    if not ncu:
+        roofline.setdefault("traffic", None)
+        return
+    roofline["traffic"] = ncu.get("dram_bytes_per_launch")
+    roofline["l2_traffic"] = ncu.get("l2_bytes_per_launch")
+    if "lsu_wavefront_pct_time_weighted" in ncu:
+        roofline["limiter"] = {
+            "lsu_wavefront_pct_of_peak": ncu["lsu_wavefront_pct_time_weighted"],
+            "issue_active_pct_of_peak": ncu["issue_active_pct_time_weighted"],
+            "l2_pct_of_peak": ncu.get("l2_pct_time_weighted"),
+            "dram_pct_of_peak": ncu.get("dram_pct_time_weighted"),
+            "threads_per_inst": ncu.get("threads_per_inst_time_weighted"),
+            "ncu_kernel_ms": ncu["ncu_duration_ns_sum"] / 1e6,
+            "source": "profiles/ncu_summary.json (tools/ncu_counts.py: ncu --metrics, "
+                      "time-weighted over the count's launches)"}
 
 
 # ---------------------------------------------------------------------------
@@ -315,12 +362,14 @@ def config_sweep(kcg, peaks, ops, l2_bytes):
         t0 = time.perf_counter()
         h = kcg.DeviceGraph.from_graph(gen.load_config_graph(cid, cache=False))
         build_s = time.perf_counter() - t0
-        h.rank(strat, spec["eps"], download=False)
-        rank_ms = h.timings()["rank_ms"]
-        h.direct(download=False)
-        direct_ms = h.timings()["direct_ms"]
+        for _ in range(2):  # second pass: buffers allocated, timings warm
+            h.rank(strat, spec["eps"], download=False)
+            rank_ms = h.timings()["rank_ms"]
+            h.direct(download=False)
+            direct_ms = h.timings()["direct_ms"]
         m = h.m
         sum_io = h.dag_work()
+        phases = phase_rooflines(strat, h.n, m, rank_ms, direct_ms, peaks)
         t3 = None
         for k in spec["ks"]:
             for pv in ([False, True] if k in spec["pv_ks"] else [False]):
@@ -342,7 +391,9 @@ def config_sweep(kcg, peaks, ops, l2_bytes):
                             "roofline": roofline_entry(cid, k, h.n, m, sum_io,
                                                        tm["count_kernel_ms"], peaks, ops,
                                                        l2_bytes, pv, t3),
+                            "phase_rooflines": phases,
                             "build_s": build_s})
+                attach_ncu(out[-1]["roofline"], ncu_entry(cid, k, pv))
         h.close()
     return out
 
@@ -375,12 +426,14 @@ def config5_block(kcg, peaks, ops, l2_bytes, steps=2):
            "device_build_s": build_s}
     # device-resident phases (graph uploaded once)
     h = kcg.DeviceGraph.from_csr_ptr(n, off_p.data_ptr(), adj_p.data_ptr())
-    h.rank(strat, spec["eps"], download=False)
-    rank_ms = h.timings()["rank_ms"]
-    h.direct(download=False)
-    direct_ms = h.timings()["direct_ms"]
+    for _ in range(2):  # second pass: buffers allocated, timings warm
+        h.rank(strat, spec["eps"], download=False)
+        rank_ms = h.timings()["rank_ms"]
+        h.direct(download=False)
+        direct_ms = h.timings()["direct_ms"]
     m = h.m
     sum_io = h.dag_work()
+    blk["phase_rooflines"] = phase_rooflines(strat, n, m, rank_ms, direct_ms, peaks)
     t3, _ = h.count(3)
     for pv in (False, True):
         key = "per_vertex" if pv else "totals"
@@ -401,10 +454,7 @@ def config5_block(kcg, peaks, ops, l2_bytes, steps=2):
                     "oriented_edges_per_s": m / ((rank_ms + direct_ms + cm) / 1e3),
                     "roofline": roofline_entry(5, 4, n, m, sum_io, km, peaks, ops, l2_bytes,
                                                pv, t3)}
-        ncu = ncu_entry(5, 4) if not pv else None
-        if ncu:
-            blk[key]["roofline"]["traffic"] = ncu.get("dram_bytes_per_launch")
-            blk[key]["roofline"]["l2_traffic"] = ncu.get("l2_bytes_per_launch")
+        attach_ncu(blk[key]["roofline"], ncu_entry(5, 4, pv))
         if gold.get("t_count_s"):
             ref_s = gold["t_count_s"] + golden.get("t_rank_s", 0) + golden.get("t_direct_s", 0)
             blk[key]["cpu_baseline"] = {
@@ -518,9 +568,8 @@ def run_kcg(args):
     roofline = roofline_entry(args.config, k, g.n, g.m, sum_io, phase["count_kernel_ms"],
                               peaks, ops, l2_bytes)
     ncu = ncu_entry(args.config, k)
+    attach_ncu(roofline, ncu)
     roofline.update({
-        "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
-        "l2_traffic": ncu.get("l2_bytes_per_launch") if ncu else None,
         "kernel_ms": phase["count_kernel_ms"], "peaks": peaks,
         "note": "achieved = B_alg (16n+20m+4*sum indeg*outdeg) / device time of the counting "
                 "kernels (CUDA events on the library stream); BW = measured L2 read bandwidth "
@@ -642,6 +691,9 @@ def run_kcg(args):
             "total": str(total),
             "oriented_edges_per_s": g.m / (ms_per_step / 1e3),
             "phases_ms": phase,
+            "phase_rooflines": phase_rooflines(gen.gpu_strategy(spec), g.n, g.m,
+                                               phase.get("rank_ms"), phase.get("direct_ms"),
+                                               peaks),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
