@@ -1176,27 +1176,43 @@ void launch_cta(Graph& g, CtaArgs a, int gws, int nt, size_t heavy_budget, cudaS
 // Tiled heavy launch (k = 4): 512-thread CTAs, two per SM when the
 // shared-memory plan allows it.
 constexpr int HV_NT = 512;
-template <bool PV>
+// Sources above d = 2047 need ~135 KB of tiles (one CTA per SM): those CTAs
+// run 1024 threads so the SM still holds 32 warps.
+constexpr int HV_NT_BIG = 1024;
+inline int heavy_threads(uint32_t dmax) { return dmax > 2047 ? HV_NT_BIG : HV_NT; }
+
+template <bool PV, int NT, int MB>
 inline unsigned heavy_grid_t(const HeavyArgs& hv, uint32_t nitems) {
-  auto kern = count_heavy4_kernel<HV_NT, 2, PV>;
+  auto kern = count_heavy4_kernel<NT, MB, PV>;
   KCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(hv.smem_bytes)));
   int occ = 0;
-  KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, HV_NT, hv.smem_bytes));
+  KCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, hv.smem_bytes));
   return unsigned(std::min<uint64_t>(nitems, uint64_t(device().sms) * std::max(occ, 1)));
 }
 inline unsigned heavy_grid(const HeavyArgs& hv, uint32_t nitems) {
-  return hv.pv_rank ? heavy_grid_t<true>(hv, nitems) : heavy_grid_t<false>(hv, nitems);
+  if (hv.nthreads == HV_NT_BIG)
+    return hv.pv_rank ? heavy_grid_t<true, HV_NT_BIG, 1>(hv, nitems)
+                      : heavy_grid_t<false, HV_NT_BIG, 1>(hv, nitems);
+  return hv.pv_rank ? heavy_grid_t<true, HV_NT, 2>(hv, nitems)
+                    : heavy_grid_t<false, HV_NT, 2>(hv, nitems);
 }
 void launch_heavy4(Graph& g, HeavyArgs hv, cudaStream_t st) {
   const unsigned grid = heavy_grid(hv, hv.nitems);
   if (size_t(grid) * hv.slice_words * 4 > g.heavy.n) fail(KCG_ERUNTIME, "heavy arena too small");
   hv.gbase = reinterpret_cast<uint32_t*>(g.heavy.p);
   KCG_CUDA(cudaMemsetAsync(hv.work, 0, 4, st));
-  if (hv.pv_rank)
-    count_heavy4_kernel<HV_NT, 2, true><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
-  else
-    count_heavy4_kernel<HV_NT, 2, false><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+  if (hv.nthreads == HV_NT_BIG) {
+    if (hv.pv_rank)
+      count_heavy4_kernel<HV_NT_BIG, 1, true><<<grid, HV_NT_BIG, hv.smem_bytes, st>>>(hv);
+    else
+      count_heavy4_kernel<HV_NT_BIG, 1, false><<<grid, HV_NT_BIG, hv.smem_bytes, st>>>(hv);
+  } else {
+    if (hv.pv_rank)
+      count_heavy4_kernel<HV_NT, 2, true><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+    else
+      count_heavy4_kernel<HV_NT, 2, false><<<grid, HV_NT, hv.smem_bytes, st>>>(hv);
+  }
   KCG_LAUNCHED(g);
   g.stats.launches++;
 }
@@ -1439,7 +1455,8 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       // the arena is sized before the launches: the plan already says which
       // kernel (per-vertex or totals) it is for
       auto tiled_plan = [&](uint32_t dmax) {
-        HeavyArgs hv = heavy_plan(dmax, HV_NT / 32, want_pv);
+        HeavyArgs hv = heavy_plan(dmax, heavy_threads(dmax) / 32, want_pv);
+        hv.nthreads = heavy_threads(dmax);
         hv.pv_rank = want_pv ? PVR(g) : nullptr;
         return hv;
       };

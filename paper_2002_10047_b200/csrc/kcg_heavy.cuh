@@ -51,6 +51,7 @@ struct HeavyArgs {
   uint32_t off_flags, off_tile_x, off_tile_i, off_queue;  // dynamic smem offsets
   uint32_t off_pvl;    // per-vertex: u32 credits of the source's d local vertices
   uint32_t smem_bytes;
+  int nthreads;        // CTA size the plan was made for
   ull* pv_rank;        // per-vertex: global counts (rank space)
 };
 
