@@ -256,31 +256,75 @@ __device__ __forceinline__ void smem_bitonic(uint32_t* a, uint32_t np2, uint32_t
     }
 }
 
-constexpr uint32_t kMidSort = 256, kBigSort = 8192;
+// Bitonic sort of 32*E keys held E per lane (key index = lane*E + r): the
+// j < E stages exchange registers of one lane, the others one shuffle per
+// key; no shared memory, no barriers.
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint32_t (&a)[E], uint32_t lane) {
+#pragma unroll
+  for (uint32_t k = 2; k <= 32u * E; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j < uint32_t(E)) {
+#pragma unroll
+        for (uint32_t r = 0; r < uint32_t(E); r++) {
+          if ((r & j) == 0) {
+            const bool asc = k < uint32_t(E) ? (r & k) == 0 : ((lane * E + r) & k) == 0;
+            const uint32_t lo = min(a[r], a[r ^ j]), hi = max(a[r], a[r ^ j]);
+            a[r] = asc ? lo : hi;
+            a[r ^ j] = asc ? hi : lo;
+          }
+        }
+      } else {
+        const uint32_t lj = j / E;
+        const bool keep_min = ((lane & lj) == 0) == (((lane * E) & k) == 0);
+#pragma unroll
+        for (uint32_t r = 0; r < uint32_t(E); r++) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, a[r], lj);
+          a[r] = keep_min ? min(a[r], y) : max(a[r], y);
+        }
+      }
+    }
+  }
+}
 
-// Relabelled slices of 33..256 targets: one warp each, in per-warp smem.
+template <int E>
+__device__ __forceinline__ void warp_sort_slice(uint32_t* __restrict__ p, uint32_t len,
+                                                uint32_t lane) {
+  uint32_t a[E];
+#pragma unroll
+  for (int r = 0; r < E; r++) a[r] = 32 * r + lane < len ? p[32 * r + lane] : 0xffffffffu;
+  warp_sort_regs<E>(a, lane);
+#pragma unroll
+  for (int r = 0; r < E; r++)
+    if (lane * E + r < len) p[lane * E + r] = a[r];
+}
+
+// Relabelled slices of 33..1024 targets: one warp each, sorted in registers
+// (8, 16 or 32 keys per lane).  Longer slices are left to sort_big_kernel.
+constexpr uint32_t kWarpSortMax = 1024;
 __global__ void __launch_bounds__(256)
-    sort_mid_kernel(const uint32_t* __restrict__ list, uint32_t nl,
-                    const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
-  __shared__ uint32_t sm[8][kMidSort];
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    sort_warp_kernel(const uint32_t* __restrict__ list, uint32_t nl,
+                     const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
+  const uint32_t lane = threadIdx.x & 31;
   for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl;
        li += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t r = list[li];
     const uint64_t b = off[r];
     const uint32_t len = uint32_t(off[r + 1] - b);
-    uint32_t np2 = 64;
-    while (np2 < len) np2 <<= 1;
-    uint32_t* a = sm[wib];
-    for (uint32_t i = lane; i < np2; i += 32) a[i] = i < len ? adj[b + i] : 0xffffffffu;
-    __syncwarp();
-    smem_bitonic(a, np2, lane, 32, [] __device__() { __syncwarp(); });
-    for (uint32_t i = lane; i < len; i += 32) adj[b + i] = a[i];
+    if (len <= 256)
+      warp_sort_slice<8>(adj + b, len, lane);
+    else if (len <= 512)
+      warp_sort_slice<16>(adj + b, len, lane);
+    else if (len <= kWarpSortMax)
+      warp_sort_slice<32>(adj + b, len, lane);
     __syncwarp();
   }
 }
 
-// Slices of 257..8192 targets: one CTA each.
+constexpr uint32_t kMidSort = 256, kBigSort = 8192;
+
+// Slices of 1025..8192 targets: one CTA each.
 __global__ void __launch_bounds__(512)
     sort_big_kernel(const uint32_t* __restrict__ list, uint32_t nl,
                     const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
@@ -289,6 +333,7 @@ __global__ void __launch_bounds__(512)
     const uint32_t r = list[li];
     const uint64_t b = off[r];
     const uint32_t len = uint32_t(off[r + 1] - b);
+    if (len <= kWarpSortMax) continue;  // sort_warp_kernel
     uint32_t np2 = 512;
     while (np2 < len) np2 <<= 1;
     for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
@@ -429,14 +474,19 @@ void build_dag(Graph& g, bool want_id_dag) {
   KCG_CUDA(cudaMemcpyAsync(hcnt, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
   g.sync();
   if (hcnt[0]) {  // 33..256 targets: a warp per slice
-    sort_mid_kernel<<<std::min<unsigned>((hcnt[0] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
+    sort_warp_kernel<<<std::min<unsigned>((hcnt[0] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
         lists, hcnt[0], g.rdag_off.p, g.rdag_adj.p);
     KCG_LAUNCHED(g);
   }
   if (hcnt[1]) {  // longer slices, listed from the back of `lists`
     const uint32_t* big = lists + n - hcnt[1];
     uint32_t maxlen = uint32_t(std::min<uint64_t>(g.max_out, 0xffffffffu));
-    if (maxlen <= kBigSort) {
+    sort_warp_kernel<<<std::min<unsigned>((hcnt[1] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
+        big, hcnt[1], g.rdag_off.p, g.rdag_adj.p);  // 257..1024 targets
+    KCG_LAUNCHED(g);
+    if (maxlen <= kWarpSortMax) {
+      // nothing longer than the warp sort takes
+    } else if (maxlen <= kBigSort) {
       sort_big_kernel<<<std::min<unsigned>(hcnt[1], 148u * 4u), 512, 0, g.stream>>>(
           big, hcnt[1], g.rdag_off.p, g.rdag_adj.p);
       KCG_LAUNCHED(g);
