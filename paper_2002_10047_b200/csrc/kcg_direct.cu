@@ -303,6 +303,9 @@ __device__ __forceinline__ void warp_sort_slice(uint32_t* __restrict__ p, uint32
 // Relabelled slices of 33..1024 targets: one warp each, sorted in registers
 // (8, 16 or 32 keys per lane).  Longer slices are left to sort_big_kernel.
 constexpr uint32_t kWarpSortMax = 1024;
+// EMAX = 8: the list holds slices of <= 256 targets only (the kernel then
+// needs few registers and runs at full occupancy); 32: up to kWarpSortMax.
+template <int EMAX>
 __global__ void __launch_bounds__(256)
     sort_warp_kernel(const uint32_t* __restrict__ list, uint32_t nl,
                      const uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
@@ -312,12 +315,14 @@ __global__ void __launch_bounds__(256)
     const uint32_t r = list[li];
     const uint64_t b = off[r];
     const uint32_t len = uint32_t(off[r + 1] - b);
-    if (len <= 256)
+    if (len <= 256) {
       warp_sort_slice<8>(adj + b, len, lane);
-    else if (len <= 512)
-      warp_sort_slice<16>(adj + b, len, lane);
-    else if (len <= kWarpSortMax)
-      warp_sort_slice<32>(adj + b, len, lane);
+    } else if constexpr (EMAX > 8) {
+      if (len <= 512)
+        warp_sort_slice<16>(adj + b, len, lane);
+      else if (len <= kWarpSortMax)
+        warp_sort_slice<32>(adj + b, len, lane);
+    }
     __syncwarp();
   }
 }
@@ -474,14 +479,14 @@ void build_dag(Graph& g, bool want_id_dag) {
   KCG_CUDA(cudaMemcpyAsync(hcnt, cnt, 8, cudaMemcpyDeviceToHost, g.stream));
   g.sync();
   if (hcnt[0]) {  // 33..256 targets: a warp per slice
-    sort_warp_kernel<<<std::min<unsigned>((hcnt[0] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
+    sort_warp_kernel<8><<<std::min<unsigned>((hcnt[0] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
         lists, hcnt[0], g.rdag_off.p, g.rdag_adj.p);
     KCG_LAUNCHED(g);
   }
   if (hcnt[1]) {  // longer slices, listed from the back of `lists`
     const uint32_t* big = lists + n - hcnt[1];
     uint32_t maxlen = uint32_t(std::min<uint64_t>(g.max_out, 0xffffffffu));
-    sort_warp_kernel<<<std::min<unsigned>((hcnt[1] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
+    sort_warp_kernel<32><<<std::min<unsigned>((hcnt[1] + 7) / 8, 148u * 16u), 256, 0, g.stream>>>(
         big, hcnt[1], g.rdag_off.p, g.rdag_adj.p);  // 257..1024 targets
     KCG_LAUNCHED(g);
     if (maxlen <= kWarpSortMax) {
