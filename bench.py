@@ -15,6 +15,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import subprocess
 import json
 import os
 import statistics
@@ -231,6 +232,23 @@ def phase_rooflines(strat, n, m, rank_ms, direct_ms, peaks):
                          "bound": "hbm", "achieved": db / (direct_ms / 1e3) / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": db / (direct_ms / 1e3) / 1e9 / hbm}
     return out
+
+
+def cpp_api_e2e(cfg_id, steps, pv=False):
+    """The reference's own call sequence through the drop-in C++ API with host
+    objects in and out (tests/cpp/api_bench.cpp over libkclique_b200.so):
+    make_ranking -> direct_by_ranking -> count_*; cold = a fresh Graph per
+    step (CSR uploaded inside the timed region), warm = the same Graph found
+    resident on the device.  Separate process: it owns its own handles."""
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", "api_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "tests/cpp/bin/api_bench not built"}
+    try:
+        out = subprocess.run([exe, str(cfg_id), str(steps), "1" if pv else "0"],
+                             capture_output=True, text=True, timeout=900, check=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError) as e:
+        return {"unavailable": f"api_bench failed: {e}"[:200]}
 
 
 def ncu_entry(cfg_id, k, pv=False):
@@ -635,6 +653,14 @@ def run_kcg(args):
     if world == 1 and not args.no_config5:
         c5 = config5_block(kcg, peaks, ops, l2_bytes)
 
+    # the same sequence through the reference's C++ headers (drop-in library)
+    api = None
+    if world == 1 and not args.no_sweep:
+        api = {"config2": cpp_api_e2e(2, 5)}
+        if not args.no_config5:
+            api["config5"] = cpp_api_e2e(5, 2)
+            api["config5_per_vertex"] = cpp_api_e2e(5, 1, True)
+
     # e2e: the reference-facing C ABI with host buffers (pinned), H2D + D2H
     # inside the timed region
     e2e = None
@@ -697,6 +723,7 @@ def run_kcg(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_cpp_api": api,
             "gpu_launches": launches,
             "clocks": clk,
             "count_stats": stats,
