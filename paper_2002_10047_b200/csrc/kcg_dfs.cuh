@@ -39,7 +39,13 @@ struct Stacks {
 // counters are flushed to 64-bit per problem.
 typedef uint32_t pvc_t;
 
-constexpr int DFS_STEPS = 8;  // steps between steal checks
+// Steps between steal checks.  The per-vertex engine carries more state per
+// step and profits from rebalancing sooner (config 4 k=6 per-vertex: 234 ms
+// at 16, 135 at 8, 91 at 4, 99 at 1); totals are best at 8.
+template <bool PV>
+constexpr int dfs_steps() {
+  return PV ? 4 : 8;
+}
 
 // Per-vertex credit of leaf nodes, transposed: every lane that created a
 // leaf node N this step broadcasts it and lane v adds its degree inside N
@@ -121,7 +127,7 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
   pvc_t lsum = 0;
   for (;;) {
 #pragma unroll
-    for (int t = 0; t < DFS_STEPS; t++) {
+    for (int t = 0; t < dfs_steps<PV>(); t++) {
       if (lJ) {
         const int y = __ffs(lJ) - 1;
         lJ &= lJ - 1;
