@@ -422,7 +422,7 @@ __device__ ull compact_count(const WarpCtx& c, const uint32_t* S, uint32_t s, in
     ct = lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv, lane);  // R == 3
   } else {
     ct = R == 3 ? lane_pairs<PV>(lane < s, c.cusym[lane], lane, c.cusym, c.csym, c.cpv, lane)
-                : steal_count<PV, MAXL>(lane < s, c.cusym[lane], R - 1, lane, c.cusym, c.csym,
+                : steal_count<PV, MAXL, true>(lane < s, c.cusym[lane], R - 1, lane, c.cusym, c.csym,
                                         c.cpv, *reinterpret_cast<Stacks<PV, MAXL>*>(c.stk),
                                         c.cand, lane);
   }

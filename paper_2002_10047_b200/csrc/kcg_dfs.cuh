@@ -42,9 +42,11 @@ typedef uint32_t pvc_t;
 // Steps between steal checks.  The per-vertex engine carries more state per
 // step and profits from rebalancing sooner (config 4 k=6 per-vertex: 234 ms
 // at 16, 135 at 8, 91 at 4, 99 at 1); totals are best at 8.
-template <bool PV>
+// CTA: the call from the CTA tier's compacted sets (short, skewed
+// problems: config 3 k=6 84.4 -> 80.8 ms at 4).
+template <bool PV, bool CTA>
 constexpr int dfs_steps() {
-  return PV ? 4 : 8;
+  return (PV || CTA) ? 4 : 8;
 }
 
 // Per-vertex credit of leaf nodes, transposed: every lane that created a
@@ -97,7 +99,7 @@ __device__ __forceinline__ uint32_t upper_split(uint32_t I) {
 // lane's root set N0; root_v is the lane's chain vertex for PV.  Returns
 // this lane's share of the total.  Must be called by all 32 lanes; `map`
 // is 32 words of warp-private shared memory.
-template <bool PV, int MAXL>
+template <bool PV, int MAXL, bool CTA = false>
 __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
                            const uint32_t* usym, const uint32_t* sym, pvc_t* cpv,
                            Stacks<PV, MAXL>& st, uint32_t* map, uint32_t lane) {
@@ -127,7 +129,7 @@ __device__ ull steal_count(bool active, uint32_t N0, int R, uint32_t root_v,
   pvc_t lsum = 0;
   for (;;) {
 #pragma unroll
-    for (int t = 0; t < dfs_steps<PV>(); t++) {
+    for (int t = 0; t < dfs_steps<PV, CTA>(); t++) {
       if (lJ) {
         const int y = __ffs(lJ) - 1;
         lJ &= lJ - 1;
