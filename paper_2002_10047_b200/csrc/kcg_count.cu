@@ -1455,8 +1455,15 @@ uint64_t count_cliques(Graph& g, int k, bool want_pv, uint32_t r_lo, uint32_t r_
       // the arena is sized before the launches: the plan already says which
       // kernel (per-vertex or totals) it is for
       auto tiled_plan = [&](uint32_t dmax) {
-        HeavyArgs hv = heavy_plan(dmax, heavy_threads(dmax) / 32, want_pv);
-        hv.nthreads = heavy_threads(dmax);
+        int nt = heavy_threads(dmax);
+        HeavyArgs hv = heavy_plan(dmax, nt / 32, want_pv);
+        if (hv.smem_bytes > smem_cap && nt != HV_NT) {
+          // 32 flag rows of a near-4095 source no longer fit next to the table
+          nt = HV_NT;
+          hv = heavy_plan(dmax, nt / 32, want_pv);
+        }
+        if (hv.smem_bytes > smem_cap) fail(KCG_ERUNTIME, "tiled plan exceeds shared memory");
+        hv.nthreads = nt;
         hv.pv_rank = want_pv ? PVR(g) : nullptr;
         return hv;
       };
