@@ -233,14 +233,16 @@ const Graph* G(const kcg_graph* h) {
 }
 
 // Large transfers between the device and PAGEABLE host memory (the drop-in
-// API's std::vectors) pin the host range for the duration of the copy
+// API's std::vectors) can pin the host range for the duration of the copy
 // (cudaHostRegister) so that it runs as one direct DMA instead of the
-// driver's staged pageable path; memory the caller already pinned is used
-// as is.  KCG_REGISTER=0 keeps the plain pageable copy.
+// driver's staged pageable path.  Off by default: on the B200 box pinning and
+// unpinning cost more than they save (api_bench, config 2: warm sequence
+// 41.3 ms registered vs 27.1 ms pageable; config 5: 1962 vs 1581 ms).
+// KCG_REGISTER=1 turns it on; memory the caller already pinned is used as is.
 bool register_host() {
   static const bool on = [] {
     const char* e = getenv("KCG_REGISTER");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
