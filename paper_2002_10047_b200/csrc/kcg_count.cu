@@ -23,9 +23,12 @@
 //                            cooperatively, sets of <= 32 vertices are
 //                            compacted (ballot transpose) to one word per
 //                            vertex and finished per lane
-//   heavy tier  d > D        the same code with the bitmap, hash and warp
-//                            scratch in a per-CTA slice of global memory
-//                            (L2-resident)
+//   heavy tier  d > D        k = 4 (D = 512): the tiled kernel of
+//                            kcg_heavy.cuh -- bitmap in a per-CTA slice of
+//                            global memory (L2), counted through 128-row
+//                            shared-memory tiles; k >= 5 (D = 1024): the
+//                            CTA-tier code with the bitmap (and, if need be,
+//                            everything else) in the global slice
 // Per-vertex counts: each task accumulates into per-source local counters
 // (u64) and flushes one global atomic per touched vertex per source.
 // Totals: warp reductions, one u64 atomic per warp.

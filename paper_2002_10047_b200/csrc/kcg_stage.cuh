@@ -23,9 +23,10 @@ constexpr int STAGE_U = 4;
 // ---------------------------------------------------------------------------
 // Row-per-warp staging with a bucketed membership table (every tier).
 //
-// The staging loop is bound by the integer ALU pipe and the shared-memory
-// crossbar (ncu: pipe_alu ~63 % of peak, lsu wavefronts next), so every
-// element costs as few ALU instructions and shared wavefronts as possible:
+// The staging loop is bound by the LSU data pipe (shared-memory and global
+// wavefronts: 75-99 % of peak before the filter words below, about two
+// thirds now) together with the issue slots (profiles/r02_notes.md), so
+// every element costs as few shared wavefronts and instructions as possible:
 //
 //  * N+(u) is hashed into B = 2^bb >= d+1 buckets of four u32 slots.  The
 //    hash h = y * mul (odd mul: a bijection of u32) names the bucket by its
@@ -37,13 +38,17 @@ constexpr int STAGE_U = 4;
 //    to B-1, the miss code).  The multiplier is chosen per source so that
 //    no bucket holds more than four keys (a few retries at most); only if
 //    eight multipliers fail does the source fall back to an overflow list
-//    (CTA-uniform flag, never taken on the benchmark graphs).
+//    (CTA-uniform flag; taken by sources whose d approaches a large B, e.g.
+//    d ~ 2000 in 2048 buckets on config 5's hubs).  After the inserts the
+//    insert counters become one filter word per bucket (bucket_filter): a
+//    probe reads the word first and only filter-positive lanes load the
+//    bucket.
 //  * Warps take whole rows N+(w_i) from a shared counter (row i is then
 //    written by one warp only) and read them 128 elements per step.  A hit
 //    writes a byte flag at its local index in the warp's flag row (plain
-//    STS.U8, no atomics: distinct indices); when the row is done, one
-//    ballot per bitmap word turns the flags into row i's words and clears
-//    them.
+//    STS.U8, no atomics: distinct indices); when the row is done, ballots
+//    turn the flags into row i's words, four per LDS.32 (flag_pos), and
+//    clear them.  The next 128 entries are always in flight (stage_scan).
 //
 // The reference's equivalent is the stamp test of counting.cpp:31-40.
 // ---------------------------------------------------------------------------
