@@ -738,6 +738,12 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
   ull* rbase = reinterpret_cast<ull*>(base + L.rbase);
   uint32_t* rowid = reinterpret_cast<uint32_t*>(base + L.rowid);
   ull* pvl = reinterpret_cast<ull*>(base + L.pvl);
+  // k = 4 per-vertex credits use the same area as u32 counters when the
+  // source allows it (a local vertex's credit is at most C(d-1, 2) < 2^32 for
+  // d <= 65536): a 32-bit shared atomic is one ATOMS.ADD where the 64-bit one
+  // is a CAS loop
+  constexpr uint32_t PV32_MAX_D = 65536;
+  uint32_t* pvl32 = reinterpret_cast<uint32_t*>(pvl);
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* wbase = base + L.warp0 + size_t(wib) * L.warp_stride;
   WarpCtx c;
@@ -838,6 +844,13 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
       // cliques (cx) and its top-vertex cliques with (i, y), i < y < x
       // (`lower`), i with its 2nd-vertex cliques (flushed per row).
       uint32_t* rc = rP;  // free after staging: row edge-count prefix
+      const bool p32 = d <= PV32_MAX_D;
+      auto credit = [&](uint32_t idx, ull val) {
+        if (p32)
+          atomicAdd(&pvl32[idx], uint32_t(val));
+        else
+          atomicAdd(&pvl[idx], val);
+      };
       const uint32_t ipt = (d + NT - 1) / NT;
       const uint32_t r0 = threadIdx.x * ipt, r1 = min(d, r0 + ipt);
       auto up_word = [&](const uint32_t* rr, uint32_t r, uint32_t w) -> uint32_t {
@@ -886,7 +899,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
             while (cur == 0) {
               if (++w >= W) {
                 if constexpr (PV) {
-                  if (ci) atomicAdd(&pvl[i], ci);
+                  if (ci) credit(i, ci);
                   ci = 0;
                 }
                 ++i;
@@ -936,7 +949,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
               }
             }
             ci += cx;
-            if (all) atomicAdd(&pvl[x], ull(all));
+            if (all) credit(x, all);
           } else {
             for (uint32_t g = w >> 2; g < G; g++) {
               const uint4 va = ri4[g], vb = rx4[g];
@@ -947,7 +960,7 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
           acc += cx;
         }
         if constexpr (PV) {
-          if (ci) atomicAdd(&pvl[i], ci);
+          if (ci) credit(i, ci);
         }
       }
       warp_src = warp_sum(acc);
@@ -985,8 +998,11 @@ __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
     }
     __syncthreads();
     if constexpr (PV) {
-      for (uint32_t i = threadIdx.x; i < d; i += NT)
-        if (pvl[i]) atomicAdd(&a.pv_rank[a.adj[b + i]], pvl[i]);
+      // (k = 4 credited the u32 view: the u64 slots were zeroed whole)
+      for (uint32_t i = threadIdx.x; i < d; i += NT) {
+        const ull v = (R == 2 && d <= PV32_MAX_D) ? ull(pvl32[i]) : pvl[i];
+        if (v) atomicAdd(&a.pv_rank[a.adj[b + i]], v);
+      }
       if (threadIdx.x == 0 && s_src_total) atomicAdd(&a.pv_rank[u], s_src_total);
     }
     __syncthreads();
