@@ -46,7 +46,6 @@ namespace {
 typedef unsigned long long ull;
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
-constexpr uint32_t NOTFOUND = 0xffffffffu;
 constexpr int WARP_THREADS_BLOCK = 256;
 constexpr int WARP_TIER_WARPS = WARP_THREADS_BLOCK / 32;
 constexpr uint32_t WARP_TABLE_BITS = 7;  // 128 buckets for <= 32 keys
@@ -715,7 +714,6 @@ constexpr int WS_TILED = 3;
 
 template <bool PV, int GWS, int NT, int MAXL, int MB>
 __global__ void __launch_bounds__(NT, MB) count_cta_kernel(CtaArgs a) {
-  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned s_src, s_edge;
   __shared__ ull s_src_total;

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-constexpr uint32_t kMidSort = 256, kBigSort = 8192;
+constexpr uint32_t kBigSort = 8192;
 
 // Slices of 1025..8192 targets: one CTA each.
 __global__ void __launch_bounds__(512)

@@ -13,8 +13,6 @@
 namespace kcg {
 namespace {
 
-constexpr ull EMPTY64 = ~0ull;
-
 __device__ __forceinline__ uint32_t popc_and4(const uint4& a, const uint4& b) {
   return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
 }
